@@ -1,0 +1,393 @@
+"""Generate golden fixtures by running the UNMODIFIED reference in this container.
+
+Run from the repo root (needs /root/reference, which is NOT on the GPU box):
+
+    python tests/golden/make_golden.py
+
+It imports ``gpuplanner`` read-only from ``/root/reference/pkg/src`` and the
+reference's own test generators from ``/root/reference/pkg/tests/support.py``
+(``random_instance`` ``support.py:190-195``, ``twelve_workload_instance``
+``support.py:232-243``, ``make_v100`` ``support.py:122-125``), runs the
+reference ``plan()`` / ``predict_gpu()`` / ``alloc_gpus()`` /
+``appropriate_batch()`` / ``_lower_bound_units()`` and freezes inputs and
+outputs as ``.npz`` files next to this script.  The fixtures are what the
+oracle is pinned against (tests/test_oracle_golden.py) and what the CUDA
+path is checked against on the GPU box (tests/test_gpu_parity.py).
+
+CPython must be 3.12+: builtin ``sum`` of floats is Neumaier-compensated
+from 3.12 on and the reference depends on it (SURVEY.md finding 1).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+
+assert sys.version_info >= (3, 12), "golden fixtures need CPython >= 3.12 (Neumaier sum)"
+
+import gpuplanner as gp  # noqa: E402
+from gpuplanner import errors as gerr  # noqa: E402
+from gpuplanner import model as gmodel  # noqa: E402
+from gpuplanner import planner as gplanner  # noqa: E402
+import support  # noqa: E402
+
+from paper_2211_01713_b200 import layout  # noqa: E402
+
+ERR_CODE = {
+    "BatchCapExceededError": layout.E_BATCH_CAP,
+    "InfeasibleSloError": layout.E_INFEASIBLE_SLO,
+    "InfeasibleResourceError": layout.E_INFEASIBLE_RES,
+    "NonPositiveDenominatorError": None,  # resolved from the message
+    "OverAllocatedError": layout.E_OVERALLOC,
+}
+
+
+def err_code(exc):
+    name = type(exc).__name__
+    if name == "NonPositiveDenominatorError":
+        return layout.E_DENOM if str(exc).startswith("r + k4") else layout.E_ACTIVE_TIME
+    return ERR_CODE[name]
+
+
+def pack_instance(workloads, hw, b_max):
+    m = len(workloads)
+    wl = np.zeros((layout.WL_NF, m), dtype=np.float64)
+    for i, (s, c) in enumerate(workloads):
+        wl[:, i] = layout.spec_coef_row(s, c)
+    names = np.array([s.name for s, _ in workloads])
+    return dict(
+        wl=wl, names=names, hw=np.array(layout.hw_vector(hw)),
+        gpu_type=np.array(hw.gpu_type), b_max=np.int64(b_max),
+    )
+
+
+def run_plan_case(workloads, hw, b_max=32):
+    """Reference plan() with stats; outputs re-indexed by input order."""
+    out = pack_instance(workloads, hw, b_max)
+    m = len(workloads)
+    stats = gplanner.PlanStats()
+    t0 = time.perf_counter()
+    try:
+        p = gp.plan(workloads, hw, b_max=b_max, stats=stats)
+    except gerr.GpuPlannerError as exc:
+        out.update(err_class=np.array(type(exc).__name__), err_msg=np.array(str(exc)),
+                   err_code=np.int64(err_code(exc)),
+                   model_evals=np.int64(stats.model_evals),
+                   candidate_gpus=np.int64(stats.candidate_gpus))
+        return out, time.perf_counter() - t0
+    dt = time.perf_counter() - t0
+    idx = {s.name: i for i, (s, _) in enumerate(workloads)}
+    gpu_of = np.full(m, -1, np.int32)
+    pos = np.full(m, -1, np.int32)
+    r = np.zeros(m)
+    units = np.zeros(m, np.int32)
+    batch = np.zeros(m, np.int32)
+    pred = np.zeros((m, layout.ROW_NF))
+    r_inter = np.zeros(m)
+    lb = np.zeros(m, np.int32)
+    for g in p.gpus:
+        for k, a in enumerate(g.allocations):
+            i = idx[a.workload]
+            gpu_of[i] = g.gpu_index
+            pos[i] = k
+            r[i] = a.r
+            units[i] = int(round(a.r / hw.r_unit))
+            assert units[i] * hw.r_unit == a.r
+            batch[i] = a.batch
+            bd = g.predicted[a.workload]
+            pred[i] = [getattr(bd, f) for f in layout.ROW_FIELDS]
+    for name, v in p.per_workload_r_inter.items():
+        r_inter[idx[name]] = v
+    for i, (s, c) in enumerate(workloads):
+        lb[i] = gplanner._lower_bound_units(s, c, hw, batch[i])
+    out.update(
+        gpu_of=gpu_of, pos=pos, r=r, units=units, batch=batch, pred=pred,
+        r_inter=r_inter, lb=lb,
+        fragment=np.array([g.fragment_r for g in p.gpus]),
+        cost=np.float64(p.cost_per_hour), gpu_count=np.int64(len(p.gpus)),
+        model_evals=np.int64(stats.model_evals),
+        candidate_gpus=np.int64(stats.candidate_gpus),
+        err_class=np.array(""), err_msg=np.array(""), err_code=np.int64(0),
+        ref_seconds=np.float64(dt),
+    )
+    return out, dt
+
+
+def simple_workload(name, k3, *, slo_ms=40.0, rate_rps=100.0):
+    # test_planner.py:37-45
+    spec = gp.WorkloadSpec(name, slo_ms, rate_rps, 0.0, 0.0)
+    coef = gp.WorkloadCoefficients(
+        n_kernels=1, k_sch_ms=0.0, k1=0.0, k2=0.0, k3=k3, k4=0.0, k5=0.0,
+        alpha_power_w=0.0, beta_power_w=10.0,
+        alpha_cacheutil=0.0, beta_cacheutil=0.0, alpha_cache=0.0,
+    )
+    return spec, coef
+
+
+def c3_feasible_workload(rng, name, hw, b_max=128):
+    """SURVEY.md §8d C3 generator: support.py:168-187 with slo U(20,100),
+    rate U(50,6000) and rejection through appropriate_batch(spec, hw, 128)."""
+    for _ in range(200):
+        spec = gp.WorkloadSpec(
+            name=name,
+            slo_ms=float(rng.uniform(20.0, 100.0)),
+            rate_rps=float(rng.uniform(50.0, 6000.0)),
+            d_load_mb=float(rng.uniform(0.05, 1.0)),
+            d_feedback_mb=float(rng.uniform(0.001, 0.05)),
+        )
+        coef = support.random_coefficients(rng)
+        try:
+            b = gp.appropriate_batch(spec, hw, b_max)
+            gp.lower_bound_resources(spec, coef, hw, b)
+        except gerr.PlanningError:
+            continue
+        return spec, coef
+    raise RuntimeError("no feasible workload")
+
+
+def wide_coef(rng):
+    """Wide coefficient draws (test_model_properties.py:25-40 ranges)."""
+    return gp.WorkloadCoefficients(
+        n_kernels=int(rng.integers(1, 501)),
+        k_sch_ms=float(rng.uniform(0.0, 0.01)),
+        k1=float(rng.uniform(0.0, 0.02)),
+        k2=float(rng.uniform(0.0, 0.2)),
+        k3=float(rng.uniform(0.0, 20.0)),
+        k4=float(rng.uniform(0.0, 2.0)),
+        k5=float(rng.uniform(1e-3, 1.0)),
+        alpha_power_w=float(rng.uniform(0.0, 100.0)),
+        beta_power_w=float(rng.uniform(0.0, 200.0)),
+        alpha_cacheutil=float(rng.uniform(0.0, 0.2)),
+        beta_cacheutil=float(rng.uniform(0.0, 0.5)),
+        alpha_cache=float(rng.uniform(0.0, 1.0)),
+    )
+
+
+def wide_spec(rng, name):
+    return gp.WorkloadSpec(
+        name, float(rng.uniform(1.0, 200.0)), float(rng.uniform(1.0, 2000.0)),
+        float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.0, 0.5)),
+    )
+
+
+def eval_states_case(rng, count, hw, nmax=12, r_unit=0.025, floor_bias=False):
+    """Random device states through the reference _eval_entries
+    (model.py:273-317); CSR layout: state s owns rows ptr[s]:ptr[s+1]."""
+    wl_rows, rs, batches, ptr, rows = [], [], [], [0], []
+    cap = int(round(1.0 / r_unit))
+    for _ in range(count):
+        n = int(rng.integers(1, nmax + 1))
+        entries, r_list = [], []
+        for k in range(n):
+            spec, coef = wide_spec(rng, f"s{k}"), wide_coef(rng)
+            if floor_bias:
+                coef = gp.WorkloadCoefficients(**{**coef.__dict__,
+                                                  "alpha_power_w": float(rng.uniform(200, 2000)),
+                                                  "beta_power_w": float(rng.uniform(100, 400))})
+            b = int(rng.integers(1, 33))
+            u = int(rng.integers(1, cap + 1))
+            r = u * r_unit if rng.random() < 0.8 else float(rng.uniform(0.001, 1.0))
+            entries.append(gmodel._Entry(spec, coef, b, hw))
+            wl_rows.append(layout.spec_coef_row(spec, coef))
+            batches.append(b)
+            r_list.append(r)
+        out = gmodel._eval_entries(entries, r_list, hw)
+        rows.extend(out)
+        rs.extend(r_list)
+        ptr.append(ptr[-1] + n)
+    return dict(
+        wl=np.array(wl_rows).T.copy(), batch=np.array(batches, np.int32),
+        r=np.array(rs), ptr=np.array(ptr, np.int64), rows=np.array(rows),
+        hw=np.array(layout.hw_vector(hw)),
+    )
+
+
+def prologue_case(rng, count, hw, b_max):
+    """appropriate_batch (planner.py:76-92) + _lower_bound_units (:95-120)
+    over wide random workloads, including every error branch."""
+    wl_rows, b_out, lb_out, code = [], [], [], []
+    for i in range(count):
+        spec = gp.WorkloadSpec(
+            f"p{i}", float(rng.uniform(0.5, 200.0)), float(rng.uniform(1.0, 8000.0)),
+            float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.0, 0.5)))
+        coef = wide_coef(rng)
+        if rng.random() < 0.1:
+            coef = gp.WorkloadCoefficients(**{**coef.__dict__, "k3": float(rng.uniform(20, 800))})
+        wl_rows.append(layout.spec_coef_row(spec, coef))
+        try:
+            b = gp.appropriate_batch(spec, hw, b_max)
+        except gerr.PlanningError as exc:
+            b_out.append(-1); lb_out.append(-1); code.append(err_code(exc))
+            continue
+        try:
+            lb = gplanner._lower_bound_units(spec, coef, hw, b)
+        except gerr.PlanningError as exc:
+            b_out.append(b); lb_out.append(-1); code.append(err_code(exc))
+            continue
+        b_out.append(b); lb_out.append(lb); code.append(0)
+    return dict(wl=np.array(wl_rows).T.copy(), batch=np.array(b_out, np.int32),
+                lb=np.array(lb_out, np.int32), code=np.array(code, np.int32),
+                hw=np.array(layout.hw_vector(hw)), b_max=np.int64(b_max))
+
+
+def alloc_case(rng, count, hw):
+    """alloc_gpus (planner.py:165-192): random residents + one newcomer."""
+    wl_rows, batch, r_in, ptr, units_out = [], [], [], [0], []
+    cap = gplanner.max_units(hw)
+    for _ in range(count):
+        inst = support.random_instance(rng, int(rng.integers(1, 9)), hw)
+        specs = {s.name: s for s, _ in inst}
+        coefs = {s.name: c for s, c in inst}
+        bs = [gp.appropriate_batch(s, hw) for s, _ in inst]
+        lbs = [gplanner._lower_bound_units(s, c, hw, b) for (s, c), b in zip(inst, bs)]
+        current = []
+        used = 0
+        for (s, _), b, lb in zip(inst[:-1], bs[:-1], lbs[:-1]):
+            u = lb + int(rng.integers(0, 3))
+            if used + u > cap - lbs[-1]:
+                break
+            used += u
+            current.append(gp.Allocation(s.name, u * hw.r_unit, b))
+        new_s = inst[-1][0]
+        res = gp.alloc_gpus(specs, coefs, hw, current, new_s.name, bs[-1],
+                            lbs[-1] * hw.r_unit)
+        names = [a.workload for a in current] + [new_s.name]
+        for nm, a in zip(names, res):
+            wl_rows.append(layout.spec_coef_row(specs[nm], coefs[nm]))
+            batch.append(a.batch)
+            units_out.append(int(round(a.r / hw.r_unit)))
+        r_in.extend([a.r for a in current] + [lbs[-1] * hw.r_unit])
+        ptr.append(ptr[-1] + len(names))
+    return dict(wl=np.array(wl_rows).T.copy(), batch=np.array(batch, np.int32),
+                r=np.array(r_in), ptr=np.array(ptr, np.int64),
+                units=np.array(units_out, np.int32), hw=np.array(layout.hw_vector(hw)))
+
+
+def denom_error_workload(name, k4, k3=-1.0, slo=40.0):
+    spec = gp.WorkloadSpec(name, slo, 100.0, 0.1, 0.01)
+    coef = gp.WorkloadCoefficients(
+        n_kernels=10, k_sch_ms=0.001, k1=0.0, k2=0.0, k3=k3, k4=k4, k5=0.2,
+        alpha_power_w=10.0, beta_power_w=20.0, alpha_cacheutil=0.02,
+        beta_cacheutil=0.05, alpha_cache=0.1)
+    return spec, coef
+
+
+def main():
+    manifest = {}
+    v100 = support.make_v100()
+
+    def save(name, d, note):
+        np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+        manifest[name] = note
+        print(f"{name}: {note}", flush=True)
+
+    # ---- plan() cases -------------------------------------------------
+    plan_cases = []
+    plan_cases.append(("plan_c1_twelve", support.twelve_workload_instance(), v100, 32,
+                       "C1: twelve_workload_instance on make_v100 (support.py:106-151)"))
+    plan_cases.append(("plan_c1_twelve_reversed",
+                       list(reversed(support.twelve_workload_instance())), v100, 32,
+                       "C1 reversed input order (test_planner.py:208-213)"))
+    rng = np.random.default_rng(7)
+    for m in (20, 40, 80):  # test_planner.py:225-234 draws these sequentially
+        plan_cases.append((f"plan_rand{m}_seq7", support.random_instance(rng, m, v100), v100, 32,
+                           f"random_instance m={m}, shared default_rng(7) stream"))
+    plan_cases.append(("plan_single", [(support.demo_spec(), support.demo_coef())], v100, 32,
+                       "test_planner.py:161-167"))
+    coef2 = support.demo_coef(alpha_cache=0.0, alpha_power_w=5.0, beta_power_w=20.0)
+    plan_cases.append(("plan_two_copies", [(support.demo_spec("a"), coef2),
+                                           (support.demo_spec("b"), coef2)], v100, 32,
+                       "test_planner.py:169-181"))
+    plan_cases.append(("plan_simple12_v100", [simple_workload(f"w{i:02d}", 9.9) for i in range(12)],
+                       v100, 32, "test_planner.py:238-243 (6 GPUs, $18.36)"))
+    t4 = gp.HardwareProfile("t4", 70.0, 1590.0, 10.0, 10.0, -1.0, 0.00475, -0.00902,
+                            price_per_hour=0.526)
+    plan_cases.append(("plan_simple15_t4", [simple_workload(f"w{i:02d}", 19.8) for i in range(15)],
+                       t4, 32, "test_planner.py:245-250 (15 GPUs, $7.89)"))
+    plan_cases.append(("plan_rand1k_seed7", support.random_instance(np.random.default_rng(7), 1000, v100),
+                       v100, 32, "C2: random_instance(default_rng(7), 1000), r_unit 0.025"))
+    plan_cases.append(("plan_rand1k_seed1", support.random_instance(np.random.default_rng(1), 1000, v100),
+                       v100, 32, "C2: random_instance(default_rng(1), 1000), r_unit 0.025"))
+    hw01 = support.make_v100(r_unit=0.01)
+    plan_cases.append(("plan_rand600_r01", support.random_instance(np.random.default_rng(3), 600, hw01),
+                       hw01, 32, "random_instance(default_rng(3), 600), r_unit 0.01 (cap 100)"))
+    rng3 = np.random.default_rng(2211)
+    c3 = [c3_feasible_workload(rng3, f"w{i:06d}", hw01) for i in range(800)]
+    plan_cases.append(("plan_c3style_800", c3, hw01, 128,
+                       "C3 generator (slo U(20,100), rate U(50,6000), b<=128, r_unit 0.01), 800 workloads"))
+    # names whose string order differs from numeric order (SURVEY finding 9)
+    rngn = np.random.default_rng(11)
+    inst = support.random_instance(rngn, 400, v100)
+    perm = rngn.permutation(400)
+    inst = [(gp.WorkloadSpec(f"w{int(perm[i]) * 37 % 1009}", s.slo_ms, s.rate_rps, s.d_load_mb,
+                             s.d_feedback_mb), c) for i, (s, c) in enumerate(inst)]
+    plan_cases.append(("plan_names_mixed400", inst, v100, 32,
+                       "400 workloads, names w<k> of mixed length (string vs numeric order)"))
+    # identical workloads: every sort key ties on lb, every argmin ties on inter
+    ident = [(gp.WorkloadSpec(f"t{i}", 40.0, 300.0, 0.5, 0.01), support.demo_coef()) for i in range(60)]
+    plan_cases.append(("plan_identical60", ident, v100, 32,
+                       "60 identical workloads: sort/argmin ties resolved by name / lowest index"))
+    # hardware variants: floor binding (tiny power cap), no scheduling term
+    hw_floor = support.make_v100(power_max_w=80.0, power_idle_w=53.5, alpha_f=-8.0)
+    plan_cases.append(("plan_floor300", support.random_instance(np.random.default_rng(5), 300, hw_floor),
+                       hw_floor, 32, "tight power cap: f_min floor binds in most evaluations"))
+    # error cases
+    inst = support.random_instance(np.random.default_rng(9), 30, v100)
+    bad = gp.WorkloadSpec("impossible", 0.9, 100.0, 0.574, 0.004)
+    plan_cases.append(("plan_err_slo", inst[:10] + [(bad, support.demo_coef())] + inst[10:], v100, 32,
+                       "InfeasibleSloError (test_planner.py:215-218) after 10 good workloads"))
+    dense = gp.WorkloadSpec("dense", 1.2, 100.0, 0.574, 0.004)
+    plan_cases.append(("plan_err_res", inst[:5] + [(dense, support.demo_coef())] + inst[5:], v100, 32,
+                       "InfeasibleResourceError (test_planner.py:220-223)"))
+    capx = gp.WorkloadSpec("capx", 200.0, 2000.0, 0.0, 0.0)
+    plan_cases.append(("plan_err_batch", inst[:3] + [(capx, support.demo_coef())] + inst[3:], v100, 32,
+                       "BatchCapExceededError (test_planner.py:59-62) mid-input"))
+    # r + k4 <= 0 on a workload that enters the plan: lb*r_unit + k4 < 0
+    plan_cases.append(("plan_err_denom", inst[:12] + [denom_error_workload("neg", -0.5)] + inst[12:],
+                       v100, 32, "NonPositiveDenominatorError raised mid-plan by _eval_entries"))
+    # k_act <= 0 branch: negative gamma keeps lb small while k_act stays negative
+    spec_k, coef_k = denom_error_workload("negk", 0.05, k3=-3.0)
+    plan_cases.append(("plan_err_kact", inst[:7] + [(spec_k, coef_k)] + inst[7:], v100, 32,
+                       "NonPositiveDenominatorError (active-time variant) mid-plan"))
+    plan_cases.append(("plan_err_denom_alone", [denom_error_workload("solo_neg", -0.5)], v100, 32,
+                       "denominator error surfaced only by _build_plan/predict_gpu"))
+
+    for name, wls, hw, bmax, note in plan_cases:
+        d, dt = run_plan_case(wls, hw, bmax)
+        extra = f" [{str(d['err_class'])}]" if str(d["err_class"]) else (
+            f" -> {int(d['gpu_count'])} GPUs, evals={int(d['model_evals'])}, "
+            f"cands={int(d['candidate_gpus'])}, {dt:.2f}s")
+        save(name, d, note + extra)
+
+    # ---- component cases ------------------------------------------------
+    save("eval_states_v100", eval_states_case(np.random.default_rng(101), 1000, v100),
+         "1000 random device states, n=1..12, wide coefficients (_eval_entries rows)")
+    save("eval_states_floor", eval_states_case(np.random.default_rng(102), 600, v100, floor_bias=True),
+         "600 states biased onto the f_min floor")
+    save("eval_states_r01", eval_states_case(np.random.default_rng(103), 500, hw01, nmax=30, r_unit=0.01),
+         "500 states, r_unit 0.01, up to 30 residents")
+    save("prologue_v100", prologue_case(np.random.default_rng(104), 6000, v100, 32),
+         "6000 workloads: appropriate_batch + _lower_bound_units incl. error codes")
+    save("prologue_r01_b128", prologue_case(np.random.default_rng(105), 6000, hw01, 128),
+         "6000 workloads, r_unit 0.01, b_max 128")
+    save("alloc_v100", alloc_case(np.random.default_rng(106), 400, v100),
+         "400 alloc_gpus calls (Alg. 2) on random residents")
+
+    with open(os.path.join(HERE, "manifest.json"), "w") as fh:
+        json.dump({"python": sys.version.split()[0], "numpy": np.__version__,
+                   "cases": manifest}, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
