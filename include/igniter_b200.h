@@ -1,0 +1,175 @@
+/*
+ * igniter_b200.h -- C-ABI of the B200-native iGniter provisioning hot path.
+ *
+ * The reference (gpuplanner, pure Python) has no FFI: its drop-in surface is
+ * the Python API re-exported by pkg/src/gpuplanner/__init__.py:3-92.  Each
+ * entry point below replaces the computation behind one of those calls; the
+ * Python host layer (paper_2211_01713_b200/) keeps the reference signatures
+ * and binds these symbols with ctypes (INTEGRATION.md shows the binding).
+ *
+ *   igp_plan_batch_device / igp_plan_batch_host
+ *       replaces plan()            planner.py:258-325  (Alg. 1 + Alg. 2 +
+ *                                  _build_plan planner.py:218-246), for one
+ *                                  or many independent scenarios
+ *   igp_eval_states_device
+ *       replaces _eval_entries     model.py:273-317 and predict_gpu
+ *                                  model.py:320-343 (batched device states)
+ *   igp_alloc_units_device
+ *       replaces _alloc_units      planner.py:133-162 behind alloc_gpus
+ *                                  planner.py:165-192
+ *   igp_prologue_device
+ *       replaces appropriate_batch planner.py:76-92 and _lower_bound_units
+ *                                  planner.py:95-120 (lower_bound_resources
+ *                                  planner.py:123-130)
+ *
+ * Conventions
+ *   - plain pointers and sizes only; "device" entry points take device
+ *     pointers and a cudaStream_t passed as void*; "host" entry points take
+ *     host pointers and synchronise before returning.
+ *   - workload tables are fp64 structure-of-arrays, field-major:
+ *     wl[f * ld + i], fields in IGP_WL_* order (16 fields).  A scenario batch
+ *     is S consecutive tables with ld = m (wl[(s * 16 + f) * m + i]).
+ *   - hardware profile: 11 doubles in IGP_HW_* order, host memory.
+ *   - result rows: 10 doubles in LatencyBreakdown order (model.py:133-146).
+ *   - every fp64 operation follows the reference's association and is
+ *     rounded separately (built with -fmad=false); builtin-sum sites use the
+ *     CPython 3.12 Neumaier fold in resident order.  Results are bit-exact.
+ *   - errors: the return value is IGP_E_OK or the first error code; the
+ *     igp_error record carries the operands the Python layer needs to raise
+ *     the reference's exception with the reference's message.
+ *   - the library keeps no pointer after a call returns; scratch lives in a
+ *     caller-owned device workspace sized by igp_plan_workspace_bytes().
+ */
+#ifndef IGNITER_B200_H
+#define IGNITER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGP_ABI_VERSION 1
+
+/* workload fields (WorkloadSpec model.py:19-27, WorkloadCoefficients model.py:40-62) */
+enum {
+  IGP_WL_SLO = 0, IGP_WL_RATE, IGP_WL_DLOAD, IGP_WL_DFB, IGP_WL_NK, IGP_WL_KSCH,
+  IGP_WL_K1, IGP_WL_K2, IGP_WL_K3, IGP_WL_K4, IGP_WL_K5, IGP_WL_ALPHA_P,
+  IGP_WL_BETA_P, IGP_WL_ALPHA_CU, IGP_WL_BETA_CU, IGP_WL_ALPHA_CACHE, IGP_WL_NF
+};
+/* hardware fields (HardwareProfile model.py:73-110) */
+enum {
+  IGP_HW_PMAX = 0, IGP_HW_FMAX, IGP_HW_PIDLE, IGP_HW_BW, IGP_HW_ALPHA_F,
+  IGP_HW_ALPHA_SCH, IGP_HW_BETA_SCH, IGP_HW_RUNIT, IGP_HW_RMAX, IGP_HW_PRICE,
+  IGP_HW_FMIN_FRAC, IGP_HW_NF
+};
+
+/* error codes -> reference exceptions (errors.py) */
+enum {
+  IGP_E_OK = 0,
+  IGP_E_BATCH_CAP = 1,      /* BatchCapExceededError  planner.py:86-91;  a = b            */
+  IGP_E_INFEASIBLE_SLO = 2, /* InfeasibleSloError     planner.py:107-111; a = delta       */
+  IGP_E_INFEASIBLE_RES = 3, /* InfeasibleResourceError planner.py:115-119; a = units      */
+  IGP_E_DENOM = 4,          /* NonPositiveDenominatorError model.py:286-290; a=denom b=r c=k4 */
+  IGP_E_ACTIVE_TIME = 5,    /* NonPositiveDenominatorError model.py:178-183; a=k_act b=batch c=r */
+  IGP_E_OVERALLOC = 6,      /* OverAllocatedError     model.py:331-335;  a = total_r b = r_max */
+  IGP_E_CAPACITY = 7,       /* a library limit was exceeded (see igp_limits)              */
+  IGP_E_CUDA = 8,           /* CUDA runtime error; a = cudaError_t                        */
+  IGP_E_ARG = 9             /* invalid argument                                           */
+};
+
+typedef struct igp_error {
+  int32_t code;
+  int32_t workload; /* input-order index of the workload the error names, or -1 */
+  int32_t gpu;      /* device index for _build_plan-time errors, or -1 */
+  int32_t pad;
+  double a, b, c;   /* message operands, see the enum above */
+} igp_error;
+
+/* plan flags */
+enum {
+  IGP_F_STATS = 1,      /* exact PlanStats (model_evals, candidate_gpus) for every
+                           scenario: no overflow early exit, no bound prune */
+  IGP_F_NO_PRED = 2,    /* skip the _build_plan breakdown rows */
+  IGP_F_CTA = 4         /* one CTA (many warps) per scenario instead of one warp:
+                           lower latency for single large plans */
+};
+
+int igp_abi_version(void);
+/* largest supported max_units(hw) = round(r_max / r_unit) */
+int igp_max_cap(void);
+/* last CUDA error string of this thread (for IGP_E_CUDA) */
+const char *igp_last_error_string(void);
+
+/* Device workspace needed by igp_plan_batch_*() for S scenarios of m workloads. */
+size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags);
+
+/*
+ * Plan S independent scenarios of m workloads each (Alg. 1, planner.py:258-325).
+ *   wl          [S][16][m] fp64
+ *   name_rank   [m] (rank_stride = 0, shared by all scenarios) or [S][m]
+ *               (rank_stride = m): rank of each name in Python string order,
+ *               the tie-break of planner.py:284
+ * outputs, all indexed by input order:
+ *   gpu_of, pos, units, batch, lb   [S][m] int32  (GPU index, position in that
+ *                                   GPU's allocation list, final units, batch,
+ *                                   lower-bound units)
+ *   pred        [S][m][10] fp64 breakdown rows (NULL or IGP_F_NO_PRED: skipped)
+ *   gpu_count   [S]
+ *   stats       [S][2] int64 {model_evals, candidate_gpus} (-1 unless IGP_F_STATS)
+ *   err         [S] igp_error
+ * returns IGP_E_OK or the first error code over scenarios (per-scenario codes
+ * are in err[s].code).
+ */
+int igp_plan_batch_device(const double *wl, int n_scen, int m, const double *hw, int b_max,
+                          const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
+                          int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
+                          double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
+                          void *workspace, size_t workspace_bytes, int flags, void *stream);
+
+/* Same contract with HOST buffers: H2D copies, kernels, D2H copies and a
+ * stream synchronisation all happen inside the call.  Pinned host memory is
+ * recommended.  workspace is device memory of igp_plan_workspace_bytes(). */
+int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw, int b_max,
+                        const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
+                        int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
+                        double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
+                        void *workspace, size_t workspace_bytes, int flags, void *stream);
+
+/*
+ * Batched device-state evaluation (_eval_entries model.py:273-317).
+ *   wl [16][n_rows] (ld = n_rows), batch [n_rows], r [n_rows], ptr [n_states+1]
+ *   rows [n_rows][10]; err [n_states] (first error of each state, in entry order)
+ *   check_capacity != 0 adds predict_gpu's Neumaier capacity check
+ *   (model.py:331-335) before the evaluation.
+ * returns the first error over states (state order).
+ */
+int igp_eval_states_device(const double *wl, int n_rows, const int32_t *batch,
+                           const double *r, const int64_t *ptr, int n_states,
+                           const double *hw, int check_capacity, double *rows,
+                           igp_error *err, void *stream);
+
+/*
+ * Batched Alg. 2 (_alloc_units planner.py:133-162) for alloc_gpus
+ * (planner.py:165-192): units start at int(round(r / r_unit)); the result may
+ * sum beyond max_units (the reference's infeasibility marker).
+ */
+int igp_alloc_units_device(const double *wl, int n_rows, const int32_t *batch,
+                           const double *r, const int64_t *ptr, int n_states,
+                           const double *hw, int32_t *units, igp_error *err, void *stream);
+
+/*
+ * appropriate_batch (planner.py:76-92) and _lower_bound_units (:95-120) for m
+ * workloads.  batch_in may be NULL (compute the batch) or supply the batch
+ * (lower_bound_resources semantics, planner.py:123-130).  code[i] is 0 or the
+ * error code of workload i (batch error before lb error).
+ */
+int igp_prologue_device(const double *wl, int m, const double *hw, int b_max,
+                        const int32_t *batch_in, int32_t *batch, int32_t *lb, int32_t *code,
+                        igp_error *err, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGNITER_B200_H */

@@ -1,0 +1,241 @@
+"""Array-level bridge between host numpy buffers and the C-ABI.
+
+PyTorch is used only as plumbing: device allocations, the current CUDA stream
+and pinned host staging.  Every computation happens in the sm_100a kernels of
+``csrc/igniter_kernels.cu``; nothing here computes model values.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .layout import HW_NF, WL_NF
+
+_ws_cache: dict = {}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(device=None):
+    torch = _torch()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _to_dev(a: np.ndarray, device):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _np_ptr(a) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else ctypes.c_void_p(0)
+
+
+def _stream(device):
+    return ctypes.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
+
+
+def workspace(nbytes: int, device=None, tag="plan"):
+    """A cached device byte buffer of at least nbytes (grows, never shrinks)."""
+    torch = _torch()
+    device = _dev(device)
+    key = (str(device), tag)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def hw_array(hw_vec) -> np.ndarray:
+    h = np.ascontiguousarray(np.asarray(hw_vec, dtype=np.float64))
+    assert h.shape == (HW_NF,)
+    return h
+
+
+def _check(rc: int):
+    if rc == 8:  # IGP_E_CUDA
+        raise RuntimeError(f"CUDA failure in libigniter_b200: {_native.last_error()}")
+    if rc in (7, 9):
+        from .errors import NativeError
+        raise NativeError(
+            "libigniter_b200 rejected the call "
+            + ("(capacity: max_units(hw) exceeds igp_max_cap())" if rc == 7 else "(bad argument)"))
+
+
+def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
+    lib = _native.load()
+    h = hw_array(hw_vec)
+    return int(lib.igp_plan_workspace_bytes(S, m, _np_ptr(h), b_max, flags))
+
+
+def plan_device(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True):
+    """Plan S scenarios; wl is [S,16,m] (or [16,m]) float64, rank [m] or [S,m].
+
+    Returns numpy arrays (all per scenario, input order)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.asarray(wl, dtype=np.float64)
+    if wl.ndim == 2:
+        wl = wl[None]
+    S, nf, m = wl.shape
+    assert nf == WL_NF
+    rank = np.asarray(rank, dtype=np.int32)
+    rank_stride = m if rank.ndim == 2 else 0
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d_wl = _to_dev(wl, device)
+        d_rank = _to_dev(rank, device)
+        i32 = torch.empty((5, S, max(m, 1)), dtype=torch.int32, device=device)
+        d_pred = torch.empty((S, max(m, 1), 10), dtype=torch.float64, device=device) if want_pred else None
+        d_gc = torch.empty(S, dtype=torch.int32, device=device)
+        d_st = torch.empty((S, 2), dtype=torch.int64, device=device)
+        d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
+        nbytes = plan_workspace_bytes(S, m, h, b_max, flags)
+        ws = workspace(nbytes, device)
+        rc = lib.igp_plan_batch_device(
+            _ptr(d_wl), S, m, _np_ptr(h), int(b_max), _ptr(d_rank), rank_stride,
+            _ptr(i32[0]), _ptr(i32[1]), _ptr(i32[2]), _ptr(i32[3]), _ptr(i32[4]),
+            _ptr(d_pred), _ptr(d_gc), _ptr(d_st), _ptr(d_err), _ptr(ws), ws.numel(),
+            int(flags), _stream(device))
+        _check(rc)
+        out_i = i32.cpu().numpy()[:, :, :m]
+        res = dict(gpu_of=out_i[0], pos=out_i[1], units=out_i[2], batch=out_i[3], lb=out_i[4],
+                   gpu_count=d_gc.cpu().numpy(), stats=d_st.cpu().numpy(),
+                   err=d_err.cpu().numpy().view(_native.err_dtype()).reshape(S))
+        if want_pred:
+            res["pred"] = d_pred.cpu().numpy()[:, :m]
+    return res
+
+
+def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=False, out=None):
+    """Host-buffer entry (igp_plan_batch_host): H2D, kernels, D2H, sync in one call.
+
+    `wl`/`rank` should be pinned (page-locked) numpy views for full PCIe
+    bandwidth; `out` may carry preallocated (pinned) output arrays."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    S, nf, m = wl.shape
+    rank_stride = m if rank.ndim == 2 else 0
+    h = hw_array(hw_vec)
+    if out is None:
+        out = dict(gpu_of=np.empty((S, m), np.int32), pos=np.empty((S, m), np.int32),
+                   units=np.empty((S, m), np.int32), batch=np.empty((S, m), np.int32),
+                   lb=np.empty((S, m), np.int32), gpu_count=np.empty(S, np.int32),
+                   stats=np.empty((S, 2), np.int64),
+                   err=np.zeros(S, _native.err_dtype()))
+        if want_pred:
+            out["pred"] = np.empty((S, m, 10))
+    nbytes = host_workspace_bytes(S, m, h, b_max, flags, rank_stride, want_pred)
+    with torch.cuda.device(device):
+        ws = workspace(nbytes, device, tag="host")
+        rc = lib.igp_plan_batch_host(
+            _np_ptr(wl), S, m, _np_ptr(h), int(b_max), _np_ptr(rank), rank_stride,
+            _np_ptr(out["gpu_of"]), _np_ptr(out["pos"]), _np_ptr(out["units"]),
+            _np_ptr(out["batch"]), _np_ptr(out["lb"]),
+            _np_ptr(out.get("pred")) if want_pred else ctypes.c_void_p(0),
+            _np_ptr(out["gpu_count"]), _np_ptr(out["stats"]), _np_ptr(out["err"]),
+            _ptr(ws), ws.numel(), int(flags), _stream(device))
+        if rc in (7, 8, 9):
+            _check(rc)
+    return out
+
+
+def host_workspace_bytes(S, m, hw_vec, b_max, flags, rank_stride, want_pred):
+    base = plan_workspace_bytes(S, m, hw_vec, b_max, flags)
+    Sm = S * max(m, 1)
+
+    def al(x):
+        return (x + 255) & ~255
+    extra = al(Sm * WL_NF * 8) + al((Sm if rank_stride else max(m, 1)) * 4) + al(Sm * 20)
+    extra += al(Sm * 80 if want_pred else 0) + al(S * 4) + al(S * 16)
+    extra += al(S * ctypes.sizeof(_native.IgpError))
+    return base + extra + 4096
+
+
+def eval_states(wl, batch, r, ptr, hw_vec, check_capacity=False, device=None):
+    """Batched _eval_entries rows for CSR device states."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.asarray(wl, np.float64)
+    n_rows = wl.shape[1]
+    n_states = len(ptr) - 1
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d_wl = _to_dev(wl, device)
+        d_b = _to_dev(np.asarray(batch, np.int32), device)
+        d_r = _to_dev(np.asarray(r, np.float64), device)
+        d_p = _to_dev(np.asarray(ptr, np.int64), device)
+        d_rows = torch.empty((max(n_rows, 1), 10), dtype=torch.float64, device=device)
+        d_err = torch.empty((max(n_states, 1), ctypes.sizeof(_native.IgpError)),
+                            dtype=torch.uint8, device=device)
+        rc = lib.igp_eval_states_device(_ptr(d_wl), n_rows, _ptr(d_b), _ptr(d_r), _ptr(d_p),
+                                        n_states, _np_ptr(h), int(bool(check_capacity)),
+                                        _ptr(d_rows), _ptr(d_err), _stream(device))
+        _check(rc)
+        rows = d_rows.cpu().numpy()[:n_rows]
+        err = d_err.cpu().numpy().view(_native.err_dtype()).reshape(-1)[:n_states]
+    return rows, err
+
+
+def alloc_units(wl, batch, r, ptr, hw_vec, device=None):
+    """Batched Alg. 2 (reference evaluation sequence)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.asarray(wl, np.float64)
+    n_rows = wl.shape[1]
+    n_states = len(ptr) - 1
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d_wl = _to_dev(wl, device)
+        d_b = _to_dev(np.asarray(batch, np.int32), device)
+        d_r = _to_dev(np.asarray(r, np.float64), device)
+        d_p = _to_dev(np.asarray(ptr, np.int64), device)
+        d_u = torch.empty(max(n_rows, 1), dtype=torch.int32, device=device)
+        d_err = torch.empty((max(n_states, 1), ctypes.sizeof(_native.IgpError)),
+                            dtype=torch.uint8, device=device)
+        rc = lib.igp_alloc_units_device(_ptr(d_wl), n_rows, _ptr(d_b), _ptr(d_r), _ptr(d_p),
+                                        n_states, _np_ptr(h), _ptr(d_u), _ptr(d_err),
+                                        _stream(device))
+        _check(rc)
+        units = d_u.cpu().numpy()[:n_rows]
+        err = d_err.cpu().numpy().view(_native.err_dtype()).reshape(-1)[:n_states]
+    return units, err
+
+
+def prologue(wl, hw_vec, b_max, batch_in=None, device=None):
+    """appropriate_batch / _lower_bound_units for m workloads."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.asarray(wl, np.float64)
+    m = wl.shape[1]
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d_wl = _to_dev(wl, device)
+        d_bin = _to_dev(np.asarray(batch_in, np.int32), device) if batch_in is not None else None
+        o = torch.empty((3, max(m, 1)), dtype=torch.int32, device=device)
+        d_err = torch.empty(ctypes.sizeof(_native.IgpError), dtype=torch.uint8, device=device)
+        rc = lib.igp_prologue_device(_ptr(d_wl), m, _np_ptr(h), int(b_max), _ptr(d_bin),
+                                     _ptr(o[0]), _ptr(o[1]), _ptr(o[2]), _ptr(d_err),
+                                     _stream(device))
+        _check(rc)
+        on = o.cpu().numpy()[:, :m]
+        err = d_err.cpu().numpy().view(_native.err_dtype())[0]
+    return on[0], on[1], on[2], err

@@ -1,0 +1,115 @@
+"""Exception hierarchy of the drop-in surface.
+
+Names, base classes and constructor signatures match the reference's
+``gpuplanner.errors`` (``errors.py:4-68``) so ``except`` clauses written
+against the reference keep working.  The native library reports failures as
+``IGP_E_*`` codes plus operands (include/igniter_b200.h); ``raise_native``
+turns one such record into the exception the reference raises, with the
+reference's message text.
+"""
+
+from __future__ import annotations
+
+
+class GpuPlannerError(Exception):
+    """Root of every error raised by this package."""
+
+
+class NonPositiveDenominatorError(GpuPlannerError):
+    """r + k4 (or the resulting active time) is not positive."""
+
+
+class OverAllocatedError(GpuPlannerError):
+    """A device's summed resource fractions exceed r_max."""
+
+
+class InsufficientDataError(GpuPlannerError):
+    """Calibration input too small (kept for API parity; calibration is out of scope)."""
+
+
+class DegenerateDesignError(GpuPlannerError):
+    """Rank-deficient regression design (API parity only)."""
+
+
+class ZeroVarianceError(GpuPlannerError):
+    """Constant regressor (API parity only)."""
+
+
+class PlanningError(GpuPlannerError):
+    """A workload cannot be provisioned; ``.workload`` names it."""
+
+    def __init__(self, workload: str, message: str):
+        self.workload = workload
+        super().__init__(f"{workload}: {message}")
+
+
+class InfeasibleSloError(PlanningError):
+    """Fixed latency terms already exhaust the half-SLO budget."""
+
+
+class InfeasibleResourceError(PlanningError):
+    """Even the whole device is below the solo resource lower bound."""
+
+
+class BatchCapExceededError(PlanningError):
+    """The arrival rate needs a batch beyond the cap."""
+
+
+class InfeasibleError(GpuPlannerError):
+    """No candidate satisfies the constraints."""
+
+
+class BudgetExceededError(GpuPlannerError):
+    """Enumeration budget exhausted (API parity only)."""
+
+
+class UnstableQueueError(GpuPlannerError):
+    """Replay queue diverged (API parity only)."""
+
+    def __init__(self, workload: str, depth: int, bound: int):
+        self.workload = workload
+        self.depth = depth
+        super().__init__(f"{workload}: queue depth {depth} exceeds {bound} at horizon end")
+
+
+class ProblemFormatError(GpuPlannerError):
+    """Malformed input document (API parity only)."""
+
+
+class NativeError(GpuPlannerError):
+    """The CUDA library failed for a reason that has no reference counterpart."""
+
+
+# IGP_E_* codes (include/igniter_b200.h)
+E_OK, E_BATCH_CAP, E_INFEASIBLE_SLO, E_INFEASIBLE_RES = 0, 1, 2, 3
+E_DENOM, E_ACTIVE_TIME, E_OVERALLOC, E_CAPACITY, E_CUDA, E_ARG = 4, 5, 6, 7, 8, 9
+
+
+def native_exception(code, a, b, c, *, spec=None, hw=None, b_max=None, detail=""):
+    """Build the reference exception for a native error record.
+
+    Message templates follow the reference raise sites:
+    planner.py:87-91, :107-111, :115-119; model.py:178-183, :286-290, :331-335.
+    """
+    if code == E_BATCH_CAP:
+        return BatchCapExceededError(
+            spec.name,
+            f"needs batch {int(a)} > cap {b_max}; a single replica cannot meet "
+            f"{spec.rate_rps} req/s within {spec.slo_ms} ms",
+        )
+    if code == E_INFEASIBLE_SLO:
+        return InfeasibleSloError(
+            spec.name, f"latency budget exhausted by fixed terms (delta={a:.6f} ms)")
+    if code == E_INFEASIBLE_RES:
+        return InfeasibleResourceError(
+            spec.name, f"needs {int(a) * hw.r_unit:.3f} of a device even running alone")
+    if code == E_DENOM:
+        return NonPositiveDenominatorError(
+            f"r + k4 = {a} must be positive (r={b}, k4={c})")
+    if code == E_ACTIVE_TIME:
+        return NonPositiveDenominatorError(
+            f"active time {a} ms at (batch={int(b)}, r={c}) must be positive; "
+            f"coefficients are corrupt")
+    if code == E_OVERALLOC:
+        return OverAllocatedError(f"allocated {a:.6f} exceeds r_max {hw.r_max}")
+    return NativeError(f"native error code {code}{': ' + detail if detail else ''}")

@@ -1,0 +1,236 @@
+"""Interference-aware latency model: drop-in types and device-backed evaluation.
+
+Types keep the reference's field names, defaults and validation
+(``gpuplanner/model.py:19-156``).  Evaluation of a device state --
+``_eval_entries`` (``model.py:273-317``) and ``predict_gpu``
+(``model.py:320-343``) -- runs in the sm_100a kernel ``k_eval_states``
+through ``igp_eval_states_device``; there is no host implementation.
+
+Units: latencies in ms, sizes in MB, bandwidth in MB/ms, frequency in MHz,
+power in W; rates are req/s at the API boundary.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from . import _device
+from .errors import native_exception
+from .layout import WL_NF, hw_vector, spec_coef_row
+
+
+@dataclass(frozen=True)
+class WorkloadSpec:
+    """SLO (ms), arrival rate (req/s) and per-request transfer sizes (MB)."""
+
+    name: str
+    slo_ms: float
+    rate_rps: float
+    d_load_mb: float
+    d_feedback_mb: float
+
+    def __post_init__(self):
+        if not self.name:
+            raise ValueError("workload name must be non-empty")
+        if self.slo_ms <= 0:
+            raise ValueError(f"slo_ms must be positive, got {self.slo_ms}")
+        if self.rate_rps <= 0:
+            raise ValueError(f"rate_rps must be positive, got {self.rate_rps}")
+        if self.d_load_mb < 0 or self.d_feedback_mb < 0:
+            raise ValueError("transfer sizes must be non-negative")
+
+
+@dataclass(frozen=True)
+class WorkloadCoefficients:
+    """Fitted per-workload coefficients (active time k1..k5, power/cache lines)."""
+
+    n_kernels: int
+    k_sch_ms: float
+    k1: float
+    k2: float
+    k3: float
+    k4: float
+    k5: float
+    alpha_power_w: float
+    beta_power_w: float
+    alpha_cacheutil: float
+    beta_cacheutil: float
+    alpha_cache: float
+
+    def __post_init__(self):
+        if self.n_kernels < 1:
+            raise ValueError(f"n_kernels must be >= 1, got {self.n_kernels}")
+        if self.k_sch_ms < 0:
+            raise ValueError(f"k_sch_ms must be >= 0, got {self.k_sch_ms}")
+        if self.alpha_cache < 0:
+            raise ValueError(f"alpha_cache must be >= 0, got {self.alpha_cache}")
+
+
+@dataclass(frozen=True)
+class HardwareProfile:
+    """Device coefficients, allocation granularity and hourly price."""
+
+    gpu_type: str
+    power_max_w: float
+    freq_max_mhz: float
+    power_idle_w: float
+    pcie_bw_mb_per_ms: float
+    alpha_f: float
+    alpha_sch_ms: float
+    beta_sch_ms: float
+    r_unit: float = 0.025
+    r_max: float = 1.0
+    price_per_hour: float = 1.0
+    f_min_frac: float = 0.3
+
+    def __post_init__(self):
+        if self.power_idle_w < 0 or self.power_max_w <= self.power_idle_w:
+            raise ValueError("requires power_max_w > power_idle_w >= 0")
+        if self.freq_max_mhz <= 0:
+            raise ValueError(f"freq_max_mhz must be positive, got {self.freq_max_mhz}")
+        if self.pcie_bw_mb_per_ms <= 0:
+            raise ValueError("pcie_bw_mb_per_ms must be positive")
+        if self.r_max != 1.0:
+            raise ValueError(f"r_max must be 1.0, got {self.r_max}")
+        if not 0 < self.r_unit <= self.r_max:
+            raise ValueError(f"r_unit must be in (0, {self.r_max}], got {self.r_unit}")
+        if self.price_per_hour <= 0:
+            raise ValueError("price_per_hour must be positive")
+        if not 0 < self.f_min_frac <= 1:
+            raise ValueError("f_min_frac must be in (0, 1]")
+
+    @property
+    def f_min_mhz(self) -> float:
+        return self.f_min_frac * self.freq_max_mhz
+
+
+@dataclass(frozen=True)
+class Allocation:
+    """A workload's resource fraction r and batch size on one device."""
+
+    workload: str
+    r: float
+    batch: int
+
+    def __post_init__(self):
+        if self.r <= 0:
+            raise ValueError(f"r must be positive, got {self.r}")
+        if self.batch < 1:
+            raise ValueError(f"batch must be >= 1, got {self.batch}")
+
+
+@dataclass(frozen=True)
+class LatencyBreakdown:
+    """One resident's predicted latency terms, throughput, solo power and cache."""
+
+    t_load_ms: float
+    t_sch_ms: float
+    t_act_ms: float
+    freq_mhz: float
+    t_gpu_ms: float
+    t_feedback_ms: float
+    t_inf_ms: float
+    throughput_rps: float
+    power_w: float
+    cache_util: float
+
+
+@dataclass(frozen=True)
+class SloCheck:
+    latency_ok: bool
+    throughput_ok: bool
+
+    @property
+    def ok(self) -> bool:
+        return self.latency_ok and self.throughput_ok
+
+
+def slo_check(breakdown: LatencyBreakdown, spec: WorkloadSpec) -> SloCheck:
+    """Half-SLO latency budget and arrival-rate floor (model.py:346-351)."""
+    return SloCheck(
+        latency_ok=breakdown.t_inf_ms <= spec.slo_ms / 2.0,
+        throughput_ok=breakdown.throughput_rps >= spec.rate_rps,
+    )
+
+
+class _Entry:
+    """A (spec, coefficients, batch) triple prepared for device evaluation.
+
+    Stands in for the reference's pre-reduced constants (model.py:239-270);
+    the constants themselves are formed on the device (k_build / row_entry).
+    ``t_half`` and ``rate_rps`` are kept because callers compare against them
+    (planner.py:158, oracle.py:73).
+    """
+
+    __slots__ = ("name", "batch", "spec", "coef", "t_half", "rate_rps")
+
+    def __init__(self, spec, coef, batch: int, hw=None):
+        self.name = spec.name
+        self.batch = batch
+        self.spec = spec
+        self.coef = coef
+        self.t_half = spec.slo_ms / 2.0
+        self.rate_rps = spec.rate_rps
+
+
+def _states_to_arrays(states):
+    """[(entries, rs), ...] -> SoA workload table, batch, r, CSR ptr."""
+    n = sum(len(e) for e, _ in states)
+    wl = np.empty((WL_NF, n), dtype=np.float64)
+    batch = np.empty(n, np.int32)
+    r = np.empty(n, np.float64)
+    ptr = np.zeros(len(states) + 1, np.int64)
+    k = 0
+    for s, (entries, rs) in enumerate(states):
+        for e, rv in zip(entries, rs):
+            wl[:, k] = spec_coef_row(e.spec, e.coef)
+            batch[k] = e.batch
+            r[k] = rv
+            k += 1
+        ptr[s + 1] = k
+    return wl, batch, r, ptr
+
+
+def _raise_state_error(rec, hw):
+    raise native_exception(int(rec["code"]), float(rec["a"]), float(rec["b"]),
+                           float(rec["c"]), hw=hw)
+
+
+def eval_states(states, hw, check_capacity=False):
+    """Evaluate many device states in one launch; returns a list of row lists.
+
+    Raises the first error in state order, as a sequential loop over the
+    reference's _eval_entries / predict_gpu would."""
+    if not states:
+        return []
+    wl, batch, r, ptr = _states_to_arrays(states)
+    rows, err = _device.eval_states(wl, batch, r, ptr, hw_vector(hw), check_capacity)
+    bad = np.nonzero(err["code"])[0]
+    if len(bad):
+        _raise_state_error(err[bad[0]], hw)
+    return [[tuple(float(v) for v in rows[i]) for i in range(ptr[s], ptr[s + 1])]
+            for s in range(len(states))]
+
+
+def _eval_entries(entries: Sequence[_Entry], rs: Sequence[float], hw: HardwareProfile):
+    """Device evaluation of one state; tuples in LatencyBreakdown order."""
+    if len(entries) == 0:
+        return []
+    return eval_states([(list(entries), list(rs))], hw)[0]
+
+
+def predict_gpu(
+    allocations: Sequence[Allocation],
+    specs: Mapping[str, WorkloadSpec],
+    coefs: Mapping[str, WorkloadCoefficients],
+    hw: HardwareProfile,
+) -> dict[str, LatencyBreakdown]:
+    """Every resident's breakdown under co-location (capacity check first)."""
+    if len(allocations) == 0:
+        return {}
+    entries = [_Entry(specs[a.workload], coefs[a.workload], a.batch, hw) for a in allocations]
+    rows = eval_states([(entries, [a.r for a in allocations])], hw, check_capacity=True)[0]
+    return {a.workload: LatencyBreakdown(*row) for a, row in zip(allocations, rows)}

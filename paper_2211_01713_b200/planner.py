@@ -1,0 +1,338 @@
+"""Provisioning API (drop-in for ``gpuplanner.planner``), executed on the B200.
+
+Signatures, return types, tie-breaks and exceptions follow the reference
+(``gpuplanner/planner.py:38-364``).  The work behind each call runs in the
+sm_100a library:
+
+* ``plan``              -> ``igp_plan_batch_device`` (prologue, sort, Alg. 1
+                           with Alg. 2 per candidate, _build_plan predictions)
+* ``alloc_gpus``        -> ``igp_alloc_units_device`` (Alg. 2)
+* ``appropriate_batch`` / ``lower_bound_resources`` -> ``igp_prologue_device``
+
+Host code only validates inputs (duplicate names, planner.py:249-255),
+ranks names in Python string order for the sort tie-break (planner.py:284),
+marshals structure-of-arrays buffers, and assembles the result objects.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from . import _device
+from .errors import (
+    BatchCapExceededError,
+    InfeasibleError,
+    InfeasibleResourceError,
+    InfeasibleSloError,
+    native_exception,
+)
+from .layout import E_BATCH_CAP, WL_NF, hw_vector, spec_coef_row
+from .model import (
+    Allocation,
+    HardwareProfile,
+    LatencyBreakdown,
+    WorkloadCoefficients,
+    WorkloadSpec,
+    _Entry,
+    predict_gpu,
+    slo_check,
+)
+
+DEFAULT_BATCH_CAP = 32
+IGP_F_STATS = 1
+IGP_F_CTA = 4
+
+
+@dataclass
+class GpuPlan:
+    """Allocations committed to one device, with model predictions."""
+
+    gpu_index: int
+    allocations: list[Allocation]
+    predicted: dict[str, LatencyBreakdown]
+    fragment_r: float
+
+
+@dataclass
+class Plan:
+    """Provisioning plan over devices of one GPU type."""
+
+    strategy: str
+    gpu_type: str
+    gpus: list[GpuPlan]
+    cost_per_hour: float
+    per_workload_r_inter: dict[str, float]
+    diagnostics: list[str] = field(default_factory=list)
+
+    @property
+    def gpu_count(self) -> int:
+        return len(self.gpus)
+
+
+@dataclass
+class PlanStats:
+    """Reference operation counters (planner.py:64-69): model_evals counts
+    per-resident model evaluations, candidate_gpus (workload, GPU) trials."""
+
+    model_evals: int = 0
+    candidate_gpus: int = 0
+
+
+def max_units(hw) -> int:
+    return int(round(hw.r_max / hw.r_unit))
+
+
+def _one_workload_table(spec, coef=None) -> np.ndarray:
+    wl = np.zeros((WL_NF, 1), dtype=np.float64)
+    if coef is None:
+        wl[:4, 0] = [spec.slo_ms, spec.rate_rps, spec.d_load_mb, spec.d_feedback_mb]
+        wl[4, 0] = 1.0
+    else:
+        wl[:, 0] = spec_coef_row(spec, coef)
+    return wl
+
+
+def appropriate_batch(spec: WorkloadSpec, hw: HardwareProfile,
+                      b_max: int = DEFAULT_BATCH_CAP) -> int:
+    """Eq. 19 batch (planner.py:76-92), computed by the device prologue."""
+    batch, _, code, err = _device.prologue(_one_workload_table(spec), hw_vector(hw), b_max)
+    if code[0] == E_BATCH_CAP:
+        raise native_exception(E_BATCH_CAP, float(err["a"]), 0.0, 0.0, spec=spec, hw=hw,
+                               b_max=b_max)
+    return int(batch[0])
+
+
+def _lower_bound_units(spec, coef, hw, batch: int) -> int:
+    """Eq. 20 lower bound in allocation units (planner.py:95-120)."""
+    _, lb, code, err = _device.prologue(_one_workload_table(spec, coef), hw_vector(hw),
+                                        DEFAULT_BATCH_CAP, batch_in=np.array([batch], np.int32))
+    if code[0]:
+        raise native_exception(int(code[0]), float(err["a"]), 0.0, 0.0, spec=spec, hw=hw)
+    return int(lb[0])
+
+
+def lower_bound_resources(spec, coef, hw, batch: int) -> float:
+    """Minimum solo resource fraction meeting the half-SLO (planner.py:123-130)."""
+    return _lower_bound_units(spec, coef, hw, batch) * hw.r_unit
+
+
+def alloc_gpus(
+    specs: Mapping[str, WorkloadSpec],
+    coefs: Mapping[str, WorkloadCoefficients],
+    hw: HardwareProfile,
+    current: Sequence[Allocation],
+    workload: str,
+    batch: int,
+    r_lower: float,
+) -> list[Allocation]:
+    """Alg. 2 for residents + newcomer (planner.py:165-192); a result summing
+    beyond r_max is the reference's infeasibility marker."""
+    names = [a.workload for a in current] + [workload]
+    batches = [a.batch for a in current] + [batch]
+    rs = [a.r for a in current] + [r_lower]
+    wl = np.empty((WL_NF, len(names)), dtype=np.float64)
+    for k, nm in enumerate(names):
+        wl[:, k] = spec_coef_row(specs[nm], coefs[nm])
+    units, err = _device.alloc_units(wl, np.array(batches, np.int32), np.array(rs),
+                                     np.array([0, len(names)], np.int64), hw_vector(hw))
+    if err[0]["code"]:
+        e = err[0]
+        raise native_exception(int(e["code"]), float(e["a"]), float(e["b"]), float(e["c"]), hw=hw)
+    return [Allocation(nm, int(u) * hw.r_unit, b) for nm, u, b in zip(names, units, batches)]
+
+
+def violation_diagnostics(gpus: Sequence[GpuPlan], specs: Mapping[str, WorkloadSpec]) -> list[str]:
+    """Readable SLO violations of predicted plans (planner.py:195-215)."""
+    out = []
+    for gpu in gpus:
+        for alloc in gpu.allocations:
+            spec = specs[alloc.workload]
+            bd = gpu.predicted[alloc.workload]
+            chk = slo_check(bd, spec)
+            if not chk.latency_ok:
+                out.append(f"{alloc.workload} on gpu {gpu.gpu_index}: predicted latency "
+                           f"{bd.t_inf_ms:.3f} ms exceeds half-SLO {spec.slo_ms / 2.0:.3f} ms")
+            if not chk.throughput_ok:
+                out.append(f"{alloc.workload} on gpu {gpu.gpu_index}: predicted throughput "
+                           f"{bd.throughput_rps:.1f} req/s below rate {spec.rate_rps:.1f} req/s")
+    return out
+
+
+def _build_plan(strategy, hw, placement, specs, coefs, lb_units) -> Plan:
+    """Plan from explicit (names, units, batches) per device; predictions for
+    all devices are evaluated in ONE device launch (planner.py:218-246)."""
+    cap = max_units(hw)
+    allocs_per_gpu = []
+    states = []
+    for names, units, batches in placement:
+        allocations = [Allocation(nm, u * hw.r_unit, b) for nm, u, b in zip(names, units, batches)]
+        allocs_per_gpu.append(allocations)
+        states.append(([_Entry(specs[a.workload], coefs[a.workload], a.batch, hw)
+                        for a in allocations], [a.r for a in allocations]))
+    from .model import eval_states
+    rows_per_gpu = eval_states([s for s in states if s[0]], hw, check_capacity=True)
+    gpus = []
+    r_inter: dict[str, float] = {}
+    it = iter(rows_per_gpu)
+    for index, ((names, units, batches), allocations) in enumerate(zip(placement, allocs_per_gpu)):
+        rows = next(it) if allocations else []
+        predicted = {a.workload: LatencyBreakdown(*row) for a, row in zip(allocations, rows)}
+        gpus.append(GpuPlan(index, allocations, predicted, (cap - sum(units)) * hw.r_unit))
+        for nm, u in zip(names, units):
+            r_inter[nm] = (u - lb_units[nm]) * hw.r_unit
+    return Plan(strategy=strategy, gpu_type=hw.gpu_type, gpus=gpus,
+                cost_per_hour=len(gpus) * hw.price_per_hour, per_workload_r_inter=r_inter)
+
+
+def _check_unique_names(workloads) -> None:
+    names = [s.name for s, _ in workloads]
+    if len(set(names)) != len(names):
+        dup = sorted({n for n in names if names.count(n) > 1})
+        raise ValueError(f"duplicate workload names: {dup}")
+
+
+def name_ranks(names: Sequence[str]) -> np.ndarray:
+    """Position of each name in Python string order (planner.py:284 tie-break)."""
+    order = sorted(range(len(names)), key=names.__getitem__)
+    rank = np.empty(len(names), np.int32)
+    rank[np.asarray(order, dtype=np.int64)] = np.arange(len(names), dtype=np.int32)
+    return rank
+
+
+def workload_table(workloads) -> np.ndarray:
+    """(spec, coef) pairs -> [16, m] float64 SoA table (layout.WL_FIELDS)."""
+    wl = np.empty((WL_NF, len(workloads)), dtype=np.float64)
+    for i, (s, c) in enumerate(workloads):
+        wl[:, i] = spec_coef_row(s, c)
+    return wl
+
+
+def _plan_from_arrays(res, s, workloads, hw) -> Plan:
+    """Assemble the reference Plan object from one scenario's device outputs."""
+    m = len(workloads)
+    g = int(res["gpu_count"][s])
+    gpu_of, pos, units = res["gpu_of"][s], res["pos"][s], res["units"][s]
+    batch, lb, pred = res["batch"][s], res["lb"][s], res["pred"][s]
+    members: list[list[int]] = [[] for _ in range(g)]
+    for i in np.lexsort((pos, gpu_of)):
+        members[gpu_of[i]].append(int(i))
+    cap = max_units(hw)
+    gpus, r_inter = [], {}
+    for j, mem in enumerate(members):
+        allocations, predicted, used = [], {}, 0
+        for i in mem:
+            name = workloads[i][0].name
+            u = int(units[i])
+            used += u
+            allocations.append(Allocation(name, u * hw.r_unit, int(batch[i])))
+            predicted[name] = LatencyBreakdown(*(float(v) for v in pred[i]))
+            r_inter[name] = (u - int(lb[i])) * hw.r_unit
+        gpus.append(GpuPlan(j, allocations, predicted, (cap - used) * hw.r_unit))
+    assert sum(len(mm) for mm in members) == m
+    return Plan(strategy="igniter", gpu_type=hw.gpu_type, gpus=gpus,
+                cost_per_hour=len(gpus) * hw.price_per_hour, per_workload_r_inter=r_inter)
+
+
+def _raise_plan_error(rec, workloads, hw, b_max):
+    code = int(rec["code"])
+    w = int(rec["workload"])
+    spec = workloads[w][0] if w >= 0 else None
+    raise native_exception(code, float(rec["a"]), float(rec["b"]), float(rec["c"]),
+                           spec=spec, hw=hw, b_max=b_max)
+
+
+def plan(
+    workloads: Sequence[tuple[WorkloadSpec, WorkloadCoefficients]],
+    hw: HardwareProfile,
+    *,
+    b_max: int = DEFAULT_BATCH_CAP,
+    stats: PlanStats | None = None,
+) -> Plan:
+    """Greedy minimum-interference provisioning (Alg. 1, planner.py:258-325).
+
+    Workloads are placed in descending order of their solo lower bound (names
+    break ties); each goes to the open device whose joint reallocation (Alg. 2)
+    adds the fewest units, lowest index on ties, else to a new device.  With
+    ``stats`` the device runs the reference's exact evaluation sequence and
+    the counters match the reference's PlanStats bit for bit."""
+    _check_unique_names(workloads)
+    m = len(workloads)
+    wl = workload_table(workloads)
+    rank = name_ranks([s.name for s, _ in workloads])
+    flags = IGP_F_STATS if stats is not None else 0
+    if m >= 4096:
+        flags |= IGP_F_CTA  # one CTA per plan: many warps share each step's candidates
+    res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags)
+    rec = res["err"][0]
+    if stats is not None:
+        stats.model_evals += int(res["stats"][0][0])
+        stats.candidate_gpus += int(res["stats"][0][1])
+    if int(rec["code"]):
+        _raise_plan_error(rec, workloads, hw, b_max)
+    return _plan_from_arrays(res, 0, workloads, hw)
+
+
+def plan_many(scenarios, hw: HardwareProfile, *, b_max: int = DEFAULT_BATCH_CAP,
+              stats: list | None = None) -> list:
+    """Plan independent scenarios (lists of (spec, coef) of equal length) in
+    one launch: one warp per scenario.  Returns a list with a Plan or the
+    exception instance the reference would raise for each scenario."""
+    if not scenarios:
+        return []
+    m = len(scenarios[0])
+    assert all(len(sc) == m for sc in scenarios), "scenarios must have equal workload counts"
+    for sc in scenarios:
+        _check_unique_names(sc)
+    wl = np.stack([workload_table(sc) for sc in scenarios])
+    rank = np.stack([name_ranks([s.name for s, _ in sc]) for sc in scenarios])
+    flags = IGP_F_STATS if stats is not None else 0
+    res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags)
+    out = []
+    for s, sc in enumerate(scenarios):
+        if stats is not None:
+            stats[s].model_evals += int(res["stats"][s][0])
+            stats[s].candidate_gpus += int(res["stats"][s][1])
+        rec = res["err"][s]
+        if int(rec["code"]):
+            try:
+                _raise_plan_error(rec, sc, hw, b_max)
+            except Exception as exc:  # noqa: BLE001 - returned, not swallowed
+                out.append(exc)
+            continue
+        out.append(_plan_from_arrays(res, s, sc, hw))
+    return out
+
+
+def plan_cost(p: Plan, hw: HardwareProfile) -> float:
+    """Devices times unit price (planner.py:328-330)."""
+    return len(p.gpus) * hw.price_per_hour
+
+
+def select_gpu_type(
+    workloads: Sequence[WorkloadSpec],
+    profiles: Sequence[HardwareProfile],
+    coefs_by_type: Mapping[str, Mapping[str, WorkloadCoefficients]],
+    *,
+    b_max: int = DEFAULT_BATCH_CAP,
+) -> Plan:
+    """Cheapest plan over GPU types, first profile on ties; infeasible types
+    are skipped (planner.py:333-364)."""
+    best: Plan | None = None
+    last_error: Exception | None = None
+    for hw in profiles:
+        try:
+            coefs = coefs_by_type[hw.gpu_type]
+            candidate = plan([(s, coefs[s.name]) for s in workloads], hw, b_max=b_max)
+        except KeyError as exc:
+            raise ValueError(f"missing coefficients for GPU type {hw.gpu_type}: {exc}") from exc
+        except (InfeasibleSloError, InfeasibleResourceError, BatchCapExceededError) as exc:
+            last_error = exc
+            continue
+        if best is None or candidate.cost_per_hour < best.cost_per_hour:
+            best = candidate
+    if best is None:
+        raise InfeasibleError(f"no GPU type can host all workloads ({last_error})")
+    return best

@@ -1,0 +1,251 @@
+"""CUDA path vs the reference (golden fixtures) and vs the CPU oracle.
+
+Every comparison is bit-exact: placements, units, batches, lower bounds,
+PlanStats and the fp64 breakdown rows (compared as int64 bit patterns; the
+north_star tolerance of 1e-9 relative is therefore met with margin 0).
+"""
+import numpy as np
+import pytest
+
+import golden_io as G
+from instances import (c3_instance, hw_from_golden, make_v100, random_instance,
+                       twelve_workload_instance, workloads_from_golden)
+
+import paper_2211_01713_b200 as igp
+from paper_2211_01713_b200 import _device, errors
+from paper_2211_01713_b200.layout import hw_vector
+from paper_2211_01713_b200.planner import IGP_F_CTA, IGP_F_STATS, name_ranks, workload_table
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2211_01713_b200 import _native
+    _native.load()
+
+
+def _plan_arrays_from_plan(p, workloads, r_unit):
+    idx = {s.name: i for i, (s, _) in enumerate(workloads)}
+    m = len(workloads)
+    gpu_of = np.full(m, -1, np.int32)
+    pos = np.full(m, -1, np.int32)
+    units = np.zeros(m, np.int32)
+    batch = np.zeros(m, np.int32)
+    pred = np.zeros((m, 10))
+    for g in p.gpus:
+        for k, a in enumerate(g.allocations):
+            i = idx[a.workload]
+            gpu_of[i], pos[i], batch[i] = g.gpu_index, k, a.batch
+            units[i] = int(round(a.r / r_unit))
+            bd = g.predicted[a.workload]
+            pred[i] = [bd.t_load_ms, bd.t_sch_ms, bd.t_act_ms, bd.freq_mhz, bd.t_gpu_ms,
+                       bd.t_feedback_ms, bd.t_inf_ms, bd.throughput_rps, bd.power_w, bd.cache_util]
+    return gpu_of, pos, units, batch, pred
+
+
+@pytest.mark.parametrize("with_stats", [True, False])
+@pytest.mark.parametrize("case", G.names("plan_"))
+def test_plan_api_matches_reference_golden(case, with_stats):
+    d = G.load(case)
+    wls = workloads_from_golden(d)
+    hw = hw_from_golden(d)
+    stats = igp.PlanStats() if with_stats else None
+    if str(d["err_class"]):
+        with pytest.raises(errors.GpuPlannerError) as ei:
+            igp.plan(wls, hw, b_max=int(d["b_max"]), stats=stats)
+        assert type(ei.value).__name__ == str(d["err_class"])
+        assert str(ei.value) == str(d["err_msg"])
+        if with_stats:
+            assert stats.model_evals == int(d["model_evals"])
+            assert stats.candidate_gpus == int(d["candidate_gpus"])
+        return
+    p = igp.plan(wls, hw, b_max=int(d["b_max"]), stats=stats)
+    gpu_of, pos, units, batch, pred = _plan_arrays_from_plan(p, wls, hw.r_unit)
+    np.testing.assert_array_equal(gpu_of, d["gpu_of"])
+    np.testing.assert_array_equal(pos, d["pos"])
+    np.testing.assert_array_equal(units, d["units"])
+    np.testing.assert_array_equal(batch, d["batch"])
+    np.testing.assert_array_equal(G.bits(pred), G.bits(d["pred"]))
+    assert p.cost_per_hour == float(d["cost"])
+    np.testing.assert_array_equal(G.bits([g.fragment_r for g in p.gpus]), G.bits(d["fragment"]))
+    r_inter = np.array([p.per_workload_r_inter[s.name] for s, _ in wls])
+    np.testing.assert_array_equal(G.bits(r_inter), G.bits(d["r_inter"]))
+    for g in p.gpus:
+        for a in g.allocations:
+            i = [s.name for s, _ in wls].index(a.workload)
+            assert a.r == float(d["r"][i])
+    if with_stats:
+        assert stats.model_evals == int(d["model_evals"])
+        assert stats.candidate_gpus == int(d["candidate_gpus"])
+
+
+@pytest.mark.parametrize("case", G.names("eval_states_"))
+def test_eval_states_match_reference_rows(case):
+    d = G.load(case)
+    rows, err = _device.eval_states(d["wl"], d["batch"], d["r"], d["ptr"], d["hw"])
+    assert (err["code"] == 0).all()
+    np.testing.assert_array_equal(G.bits(rows), G.bits(d["rows"]))
+
+
+@pytest.mark.parametrize("case", G.names("prologue_"))
+def test_prologue_matches_reference(case):
+    d = G.load(case)
+    b, lb, code, err = _device.prologue(d["wl"], d["hw"], int(d["b_max"]))
+    np.testing.assert_array_equal(code, d["code"])
+    np.testing.assert_array_equal(b[code != 1], d["batch"][code != 1])
+    np.testing.assert_array_equal(lb[code == 0], d["lb"][code == 0])
+    first = np.nonzero(code)[0]
+    assert int(err["workload"]) == (int(first[0]) if len(first) else -1)
+
+
+def test_alloc_units_match_reference():
+    d = G.load("alloc_v100")
+    u, err = _device.alloc_units(d["wl"], d["batch"], d["r"], d["ptr"], d["hw"])
+    assert (err["code"] == 0).all()
+    np.testing.assert_array_equal(u, d["units"])
+
+
+def _compare_to_oracle(res, s, wl, hw_vec, b_max, rank, oracle, stats=False):
+    o = oracle.plan(wl, hw_vec, b_max, rank)
+    assert o["rc"] == int(res["err"][s]["code"])
+    if o["rc"]:
+        return o
+    for k in ("gpu_of", "pos", "units", "batch", "lb"):
+        np.testing.assert_array_equal(res[k][s], o[k], err_msg=k)
+    assert int(res["gpu_count"][s]) == o["gpu_count"]
+    np.testing.assert_array_equal(G.bits(res["pred"][s]), G.bits(o["pred"]))
+    if stats:
+        assert int(res["stats"][s][0]) == o["model_evals"]
+        assert int(res["stats"][s][1]) == o["candidate_gpus"]
+    return o
+
+
+@pytest.mark.parametrize("flags", [0, IGP_F_STATS, IGP_F_CTA, IGP_F_CTA | IGP_F_STATS])
+def test_scenario_batch_vs_oracle(oracle_lib, flags):
+    hw = make_v100()
+    rng = np.random.default_rng(123)
+    scen = [random_instance(rng, 300, hw) for _ in range(12)]
+    wl = np.stack([workload_table(sc) for sc in scen])
+    rank = np.stack([name_ranks([s.name for s, _ in sc]) for sc in scen])
+    res = _device.plan_device(wl, hw_vector(hw), 32, rank, flags=flags)
+    for s in range(len(scen)):
+        _compare_to_oracle(res, s, wl[s], np.array(hw_vector(hw)), 32, rank[s], oracle_lib,
+                           stats=bool(flags & IGP_F_STATS))
+
+
+def test_plan_many_matches_single_plans():
+    hw = make_v100()
+    rng = np.random.default_rng(5)
+    scen = [random_instance(rng, 80, hw) for _ in range(6)]
+    stats = [igp.PlanStats() for _ in scen]
+    many = igp.plan_many(scen, hw, stats=stats)
+    for sc, p, st in zip(scen, many, stats):
+        st1 = igp.PlanStats()
+        q = igp.plan(sc, hw, stats=st1)
+        assert [[(a.workload, a.r, a.batch) for a in g.allocations] for g in p.gpus] == \
+               [[(a.workload, a.r, a.batch) for a in g.allocations] for g in q.gpus]
+        assert (st.model_evals, st.candidate_gpus) == (st1.model_evals, st1.candidate_gpus)
+
+
+def test_r_unit_001_and_c3_generator_vs_oracle(oracle_lib):
+    hw = make_v100(r_unit=0.01)
+    rng = np.random.default_rng(2211)
+    scen = [c3_instance(rng, 500, hw) for _ in range(4)]
+    wl = np.stack([workload_table(sc) for sc in scen])
+    rank = np.stack([name_ranks([s.name for s, _ in sc]) for sc in scen])
+    for flags in (0, IGP_F_STATS, IGP_F_CTA):
+        res = _device.plan_device(wl, hw_vector(hw), 128, rank, flags=flags)
+        for s in range(len(scen)):
+            _compare_to_oracle(res, s, wl[s], np.array(hw_vector(hw)), 128, rank[s], oracle_lib,
+                               stats=bool(flags & IGP_F_STATS))
+
+
+def test_full_size_10k_plan_vs_oracle(oracle_lib):
+    """BASELINE metric size: one 10k-workload plan, bit-exact vs the oracle."""
+    from paper_2211_01713_b200 import synth
+    hw = make_v100()
+    wl, names = synth.scenarios(1, 10_000, hw, seed=77)
+    rank = name_ranks(list(names))
+    for flags in (0, IGP_F_CTA):
+        res = _device.plan_device(wl, hw_vector(hw), 32, rank, flags=flags)
+        _compare_to_oracle(res, 0, wl[0], np.array(hw_vector(hw)), 32, rank, oracle_lib)
+
+
+def test_reference_error_messages_and_types():
+    hw = make_v100()
+    spec = igp.WorkloadSpec("w", 200.0, 2000.0, 0.0, 0.0)
+    with pytest.raises(errors.BatchCapExceededError, match="w"):
+        igp.appropriate_batch(spec, hw)
+    assert igp.appropriate_batch(spec, hw, b_max=512) == 200  # test_planner.py:64-66
+    for slo, rate, exp in [(15.0, 500.0, 4), (40.0, 400.0, 8), (60.0, 200.0, 6)]:
+        assert igp.appropriate_batch(igp.WorkloadSpec("w", slo, rate, 0.574, 0.004), hw) == exp
+    coef = igp.WorkloadCoefficients(100, 0.002, 0.001, 0.05, 0.5, 0.05, 0.2, 50.0, 60.0, 0.05, 0.10, 0.25)
+    assert igp.lower_bound_resources(igp.WorkloadSpec("resnet", 40.0, 400.0, 0.574, 0.004), coef, hw, 8) == 0.025
+    assert igp.lower_bound_resources(igp.WorkloadSpec("w", 22.0, 400.0, 0.574, 0.004), coef, hw, 8) == 0.05
+    with pytest.raises(errors.InfeasibleSloError, match="w"):
+        igp.lower_bound_resources(igp.WorkloadSpec("w", 1.2, 400.0, 0.574, 0.004), coef, hw, 8)
+
+
+def test_predict_gpu_known_values_and_overallocation():
+    hw = make_v100()
+    spec = igp.WorkloadSpec("resnet", 40.0, 400.0, 0.574, 0.004)
+    coef = igp.WorkloadCoefficients(100, 0.002, 0.001, 0.05, 0.5, 0.05, 0.2, 50.0, 60.0, 0.05, 0.10, 0.25)
+    bd = igp.predict_gpu([igp.Allocation("resnet", 0.025, 8)], {"resnet": spec}, {"resnet": coef}, hw)["resnet"]
+    assert bd.t_gpu_ms == pytest.approx(13.253333333333334, rel=1e-12)   # test_model.py:153-160
+    assert bd.t_inf_ms == pytest.approx(13.715733333333333, rel=1e-12)
+    assert bd.freq_mhz == 1530.0
+    assert bd.throughput_rps == pytest.approx(603.4760218860637, rel=1e-12)
+    assert igp.predict_gpu([], {}, {}, hw) == {}
+    other = igp.WorkloadSpec("other", 40.0, 400.0, 0.574, 0.004)
+    with pytest.raises(errors.OverAllocatedError):
+        igp.predict_gpu([igp.Allocation("resnet", 0.6, 8), igp.Allocation("other", 0.45, 8)],
+                        {"resnet": spec, "other": other}, {"resnet": coef, "other": coef}, hw)
+    bad = igp.WorkloadCoefficients(100, 0.002, 0.001, 0.05, 0.5, -0.5, 0.2, 50.0, 60.0, 0.05, 0.10, 0.25)
+    with pytest.raises(errors.NonPositiveDenominatorError, match="r \\+ k4"):
+        igp.predict_gpu([igp.Allocation("resnet", 0.3, 8)], {"resnet": spec}, {"resnet": bad}, hw)
+
+
+def test_boundary_corunner_alloc():
+    """test_planner.py:126-157: exact t_inf == t_half boundary."""
+    hw = make_v100(alpha_sch_ms=0.0, beta_sch_ms=0.0)
+    res_spec = igp.WorkloadSpec("resident", 40.0, 100.0, 0.0, 0.0)
+    res_coef = igp.WorkloadCoefficients(1, 0.0, 0.0, 0.0, 10.0, 0.0, 0.0, 0.0, 10.0, 0.0, 0.0, 0.5)
+    solo = igp.predict_gpu([igp.Allocation("resident", 0.5, 2)], {"resident": res_spec},
+                           {"resident": res_coef}, hw)
+    assert solo["resident"].t_inf_ms == 20.0
+    new_spec = igp.WorkloadSpec("new", 40.0, 50.0, 0.0, 0.0)
+    new_coef = igp.WorkloadCoefficients(1, 0.0, 0.0, 0.0, 0.5, 0.0, 0.0, 0.0, 10.0, 0.0, 0.3, 0.0)
+    specs = {"resident": res_spec, "new": new_spec}
+    coefs = {"resident": res_coef, "new": new_coef}
+    result = igp.alloc_gpus(specs, coefs, hw, [igp.Allocation("resident", 0.5, 2)], "new", 1, 0.025)
+    by = {a.workload: a for a in result}
+    assert by["resident"].r > 0.5
+
+
+def test_select_gpu_type_cheaper_type_wins():
+    v100 = make_v100()
+    t4 = igp.HardwareProfile("t4", 70.0, 1590.0, 10.0, 10.0, -1.0, 0.00475, -0.00902,
+                             price_per_hour=0.526)
+
+    def simple(name, k3):
+        return (igp.WorkloadSpec(name, 40.0, 100.0, 0.0, 0.0),
+                igp.WorkloadCoefficients(1, 0.0, 0.0, 0.0, k3, 0.0, 0.0, 0.0, 10.0, 0.0, 0.0, 0.0))
+    specs = [simple(f"w{i:02d}", 9.9)[0] for i in range(15)]
+    chosen = igp.select_gpu_type(specs, [v100, t4], {
+        "v100": {s.name: simple(s.name, 9.9)[1] for s in specs},
+        "t4": {s.name: simple(s.name, 19.8)[1] for s in specs}})
+    assert chosen.gpu_type == "t4" and len(chosen.gpus) == 15
+    assert round(chosen.cost_per_hour, 2) == 7.89
+
+
+def test_twelve_workload_order_invariance():
+    hw = make_v100()
+    w = twelve_workload_instance()
+    a = igp.plan(w, hw)
+    b = igp.plan(list(reversed(w)), hw)
+    assert [[(x.workload, x.r, x.batch) for x in g.allocations] for g in a.gpus] == \
+           [[(x.workload, x.r, x.batch) for x in g.allocations] for g in b.gpus]
