@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: provisioning plans/s and candidate evals/s at 10k workloads.
+
+Workload (BASELINE.json metric "provisioning plans/sec and candidate evals/sec
+at 10k workloads, 1/2/4/8 B200"): a batch of S independent provisioning
+scenarios per GPU, each 10,000 synthetic workloads drawn from the reference
+generator's distributions (C2 generator scaled to 10k: r_unit 0.025, b<=32,
+V100 profile of pkg/tests/support.py:16-33), planned with Alg. 1/Alg. 2 and
+the _build_plan predictions.  One step = one full plan of every scenario in
+the batch (prepare + place kernels).  Scenarios shard across ranks with no
+data-path collective (weak scaling); for N>1 the fixed-size plan records are
+gathered over NCCL inside the timed step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+import numpy as np  # noqa: E402
+
+M_DEFAULT = 10_000
+V100 = dict(gpu_type="v100", power_max_w=300.0, freq_max_mhz=1530.0, power_idle_w=53.5,
+            pcie_bw_mb_per_ms=10.0, alpha_f=-1.025, alpha_sch_ms=0.00475,
+            beta_sch_ms=-0.00902, r_unit=0.025, price_per_hour=3.06)
+FLOPS_PER_MODEL_EVAL = 30   # fp64 ops per resident evaluation
+FLOPS_PER_EVAL_CALL = 9     # fp64 ops per device evaluation
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scenarios", type=int, default=0, help="scenarios per GPU (0 = auto)")
+    ap.add_argument("--workloads", type=int, default=M_DEFAULT)
+    ap.add_argument("--seed", type=int, default=2211)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--flags", type=int, default=0, help="extra IGP_F_* flags")
+    return ap.parse_args()
+
+
+def hardware():
+    from paper_2211_01713_b200.model import HardwareProfile
+    return HardwareProfile(**V100)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        loaded = [v for v in sm if v > 0.5 * smax] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def fp64_peak():
+    """Measured FP64 DFMA flop/s of this GPU (tools/fp64_probe.cu)."""
+    import torch
+    path = os.path.join(REPO, "tools", "libfp64probe.so")
+    if not os.path.exists(path):
+        return None, "missing tools/libfp64probe.so"
+    lib = ctypes.CDLL(path)
+    lib.fp64_probe_flops.restype = ctypes.c_double
+    lib.fp64_probe_flops.argtypes = [ctypes.c_int, ctypes.c_int]
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return lib.fp64_probe_flops(0, sms), lib.fp64_probe_flops(1, sms)
+
+
+def cpu_reference(wl, hw_vec, b_max, rank, threads, n_scen):
+    """The CPU oracle (restatement of the reference path) on host threads."""
+    from oracle import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    r = oracle.plan_batch(wl[:n_scen], hw_vec, b_max, rank, threads, stats=False)
+    dt = time.perf_counter() - t0
+    assert r["rc"] == 0
+    return n_scen / dt, dt
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU path on all host threads (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2211_01713_b200 import synth
+    from paper_2211_01713_b200.layout import hw_vector
+    from paper_2211_01713_b200.planner import name_ranks
+    hw = hardware()
+    threads = args.cpu_threads or os.cpu_count() or 1
+    per_step = threads  # one 10k scenario per thread per step
+    wl, names = synth.scenarios(per_step, args.workloads, hw, seed=args.seed)
+    rk = name_ranks(list(names))
+    hv = np.array(hw_vector(hw))
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_reference(wl, hv, 32, rk, threads, min(threads, per_step))
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_reference(wl, hv, 32, rk, threads, per_step)
+        times.append(dt)
+    total = sum(times)
+    value = per_step * args.steps / total
+    line = {
+        "impl": "reference",
+        "metric": "provisioning plans/sec at 10k workloads",
+        "value": value, "unit": "plans/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{per_step} scenarios x {args.workloads} workloads per step "
+                               "(C2 generator, r_unit 0.025, b<=32, V100 profile)",
+                   "workloads_per_scenario": args.workloads},
+        "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} x {args.workloads}-workload plans per step, one per "
+                                   "host thread (oracle/igniter_oracle.c, pthreads)"},
+        "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    from paper_2211_01713_b200 import _device, _native, synth
+    from paper_2211_01713_b200.layout import hw_vector
+    from paper_2211_01713_b200.planner import IGP_F_STATS, name_ranks
+
+    lib = _native.lib_for_compute()
+    hw = hardware()
+    hv = np.array(hw_vector(hw))
+    b_max = 32
+    m = args.workloads
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    S = args.scenarios or sms * 16
+    flags = args.flags
+
+    # ---- synthetic inputs (different seed per rank: weak scaling) ----
+    wl_np, names = synth.scenarios(S, m, hw, seed=args.seed + 1000 * rank)
+    rk_np = name_ranks(list(names))
+    wl_pin = torch.from_numpy(wl_np).pin_memory()
+    rk_pin = torch.from_numpy(rk_np).pin_memory()
+    d_wl = wl_pin.to(device)
+    d_rk = rk_pin.to(device)
+    i32 = torch.empty((5, S, m), dtype=torch.int32, device=device)
+    d_pred = torch.empty((S, m, 10), dtype=torch.float64, device=device)
+    d_gc = torch.empty(S, dtype=torch.int32, device=device)
+    d_st = torch.empty((S, 4), dtype=torch.int64, device=device)
+    d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
+    ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, b_max, flags | IGP_F_STATS),
+                     dtype=torch.uint8, device=device)
+    stream = torch.cuda.current_stream(device)
+    P = _device._ptr
+    hp = _device._np_ptr(hv)
+
+    def call(fn, fl):
+        rc = fn(P(d_wl), S, m, hp, b_max, P(d_rk), 0, P(i32[0]), P(i32[1]), P(i32[2]), P(i32[3]),
+                P(i32[4]), P(d_pred), P(d_gc), P(d_st), P(d_err), P(ws), ws.numel(), fl,
+                ctypes.c_void_p(stream.cuda_stream))
+        assert rc == 0, rc
+
+    # ---- reference-equivalent work: one exact-stats pass (untimed) ----
+    call(lib.igp_plan_batch_device, flags | IGP_F_STATS)
+    torch.cuda.synchronize()
+    st = d_st.cpu().numpy()
+    assert (d_err.cpu().numpy().view(_native.err_dtype())["code"] == 0).all()
+    ref_model_evals = int(st[:, 0].sum())
+    ref_cands = int(st[:, 1].sum())
+    ref_calls = int(st[:, 2].sum())
+    gpus_exact = d_gc.cpu().numpy().copy()
+    units_exact = i32[2].cpu().numpy().copy()
+
+    # gather buffers for N>1: fixed-size records (gpu_of + units per workload, gpu_count)
+    if world > 1:
+        import torch.distributed as dist
+        rec = torch.empty((S, 2 * m + 1), dtype=torch.int32, device=device)
+        gathered = torch.empty((world, S, 2 * m + 1), dtype=torch.int32, device=device)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        call(lib.igp_plan_prepare_device, flags)
+        if ev is not None:
+            ev[1].record(stream)
+        call(lib.igp_plan_place_device, flags)
+        if ev is not None:
+            ev[2].record(stream)
+        if world > 1:
+            rec[:, :m].copy_(i32[0])
+            rec[:, m:2 * m].copy_(i32[2])
+            rec[:, 2 * m].copy_(d_gc)
+            dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # the fast path must reproduce the exact pass bit for bit
+    assert np.array_equal(d_gc.cpu().numpy(), gpus_exact)
+    assert np.array_equal(i32[2].cpu().numpy(), units_exact)
+    performed_calls = int(d_st.cpu().numpy()[:, 3].sum())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e_start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        e_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    clocks = clk.summary()
+    ms_total = e_start.elapsed_time(e_end)
+    place_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    prep_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    value = S * world * args.steps / (ms_total / 1e3)
+    evals_per_s = ref_model_evals * world * args.steps / (ms_total / 1e3)
+
+    # ---- e2e through the host-buffer C-ABI entry (pinned buffers, copies timed) ----
+    e2e = None
+    if not args.no_e2e:
+        wl_host = wl_pin.numpy()
+        rk_host = rk_pin.numpy()
+        out = {k: torch.empty((S, m), dtype=torch.int32).pin_memory().numpy()
+               for k in ("gpu_of", "pos", "units", "batch", "lb")}
+        out["gpu_count"] = torch.empty(S, dtype=torch.int32).pin_memory().numpy()
+        out["stats"] = torch.empty((S, 4), dtype=torch.int64).pin_memory().numpy()
+        out["err"] = np.zeros(S, _native.err_dtype())
+        del ws
+        torch.cuda.empty_cache()
+        _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device, out=out)
+        torch.cuda.synchronize()
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        ea.record(stream)
+        for _ in range(args.steps):
+            _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device, out=out)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = ea.elapsed_time(eb)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        assert np.array_equal(out["units"], units_exact)
+        h2d = wl_host.nbytes + rk_host.nbytes
+        d2h = sum(out[k].nbytes for k in ("gpu_of", "pos", "units", "batch", "lb", "gpu_count",
+                                          "stats", "err"))
+        e2e = {"value": S * world * args.steps / (e2e_ms / 1e3), "unit": "plans/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_ms / args.steps}
+
+    # ---- roofline of the dominant kernel (k_plan, the place stage) ----
+    place_avg = sum(place_ms) / len(place_ms)
+    flops_per_launch = FLOPS_PER_MODEL_EVAL * ref_model_evals + FLOPS_PER_EVAL_CALL * ref_calls
+    peak_fma, peak_add = fp64_peak()
+    achieved = flops_per_launch / (place_avg / 1e3) / 1e12
+    roofline = {
+        "bound": "fp64", "achieved": achieved,
+        "peak": (peak_fma / 1e12) if peak_fma else None, "unit": "TFLOP/s",
+        "frac": (achieved / (peak_fma / 1e12)) if peak_fma else None,
+        "traffic": None,
+        "kernel": "k_plan (igp_plan_place_device)",
+        "peak_source": "measured DFMA rate, tools/fp64_probe.cu (MEASURED_PEAKS.json has no FP64 figure)",
+        "peak_dadd_tflops": (peak_add / 1e12) if peak_add else None,
+        "flops_definition": f"{FLOPS_PER_MODEL_EVAL} x reference model_evals + "
+                            f"{FLOPS_PER_EVAL_CALL} x reference _eval_entries calls per launch",
+        "place_ms_avg": place_avg, "prepare_ms_avg": sum(prep_ms) / len(prep_ms),
+        "place_share_of_step": place_avg / (ms_total / args.steps) if world == 1 else None,
+    }
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or os.cpu_count() or 1
+        n = threads
+        wl_c, names_c = synth.scenarios(n, m, hw, seed=args.seed + 999_999)
+        v, dt = cpu_reference(wl_c, hv, b_max, name_ranks(list(names_c)), threads, n)
+        cpu = {"value": v, "unit": "plans/s", "cores": threads, "kind": "port",
+               "sample": f"{n} x {m}-workload plans, one per host thread, {dt:.1f} s "
+                         "(oracle/igniter_oracle.c restatement, pthreads)"}
+
+    if rank == 0:
+        line = {
+            "metric": "provisioning plans/sec at 10k workloads",
+            "value": value, "unit": "plans/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{S} scenarios x {m} workloads per GPU per step "
+                                  "(C2 generator scaled to 10k, r_unit 0.025, b<=32, V100 profile)",
+                       "scenarios_per_gpu": S, "workloads_per_scenario": m,
+                       "l2": "inputs larger than L2 (%.2f GB per GPU)" % (wl_np.nbytes / 1e9),
+                       "parallelism": f"scenario shards x{world}, NCCL all-gather of plan records"},
+            "candidate_evals_per_s": evals_per_s,
+            "candidate_evals_definition": "reference PlanStats.model_evals (planner.py:156-157) "
+                                          "of the planned scenarios, from an exact-stats pass",
+            "reference_counters_per_gpu_step": {"model_evals": ref_model_evals,
+                                                "candidate_gpus": ref_cands,
+                                                "eval_calls": ref_calls,
+                                                "eval_calls_run_fast_path": performed_calls},
+            "gpu_launches": 5 * args.steps * (1 if args.no_e2e else 2),
+            "clocks": clocks,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -117,12 +117,32 @@ size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, 
  *                                   lower-bound units)
  *   pred        [S][m][10] fp64 breakdown rows (NULL or IGP_F_NO_PRED: skipped)
  *   gpu_count   [S]
- *   stats       [S][2] int64 {model_evals, candidate_gpus} (-1 unless IGP_F_STATS)
+ *   stats       [S][4] int64 {model_evals, candidate_gpus, eval_calls, evals_run}:
+ *               the reference's PlanStats counters (planner.py:64-69) and its
+ *               number of _eval_entries calls -- exact with IGP_F_STATS (or for
+ *               a scenario that raised), -1 otherwise -- and the number of
+ *               device evaluations this kernel actually ran
  *   err         [S] igp_error
  * returns IGP_E_OK or the first error code over scenarios (per-scenario codes
  * are in err[s].code).
  */
 int igp_plan_batch_device(const double *wl, int n_scen, int m, const double *hw, int b_max,
+                          const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
+                          int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
+                          double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
+                          void *workspace, size_t workspace_bytes, int flags, void *stream);
+
+/* The two stages of igp_plan_batch_device, same arguments and workspace:
+ * prepare = prologue (batch, lower bound, first input-order error), the
+ * (-lb, name) sort and the per-workload entry constants; place = the Alg. 1
+ * step loop with Alg. 2 per candidate plus the _build_plan predictions.
+ * Exposed so callers can time / overlap the stages separately. */
+int igp_plan_prepare_device(const double *wl, int n_scen, int m, const double *hw, int b_max,
+                            const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
+                            int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
+                            double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
+                            void *workspace, size_t workspace_bytes, int flags, void *stream);
+int igp_plan_place_device(const double *wl, int n_scen, int m, const double *hw, int b_max,
                           const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
                           int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
                           double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,

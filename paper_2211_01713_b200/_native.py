@@ -81,6 +81,10 @@ PROTOTYPES = {
     "igp_plan_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I]),
     "igp_plan_batch_device": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP, _SZ, _I, _VP]),
+    "igp_plan_prepare_device": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP,
+                                     _VP, _VP, _VP, _VP, _VP, _SZ, _I, _VP]),
+    "igp_plan_place_device": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP,
+                                   _VP, _VP, _VP, _VP, _VP, _SZ, _I, _VP]),
     "igp_plan_batch_host": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP,
                                  _VP, _VP, _VP, _VP, _VP, _SZ, _I, _VP]),
     "igp_eval_states_device": (_I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _I, _VP, _VP, _VP]),

@@ -323,7 +323,8 @@ __device__ __forceinline__ void err_operands(const Hw &hw, const double *ce, int
 template <int MAXN>
 __device__ int run_candidate(const Hw &hw, const Scn &sc, int j, int k, int need, double tsch_new,
                              bool exact, const volatile unsigned long long *best, Cand<MAXN> &cd,
-                             int &n_out, int &sum_out, long long &evals, ErrOut &eo) {
+                             int &n_out, int &sum_out, long long &evals, long long &calls,
+                             ErrOut &eo) {
   const int cap = sc.cap;
   const int nres = sc.nres[j];
   const int n = nres + 1;
@@ -386,6 +387,7 @@ __device__ int run_candidate(const Hw &hw, const Scn &sc, int j, int k, int need
         C = fc.result();
         scale = f / hw.fmax;
         evals += n;
+        calls += 1;
         need_eval = false;
       }
       // per-resident terms (model.py:308-313); only t_inf is tested (planner.py:158)
@@ -430,8 +432,7 @@ __device__ int run_candidate(const Hw &hw, const Scn &sc, int j, int k, int need
 
 struct GroupSmem {
   unsigned long long best;
-  unsigned long long step_evals;
-  unsigned int step_cands;
+  unsigned long long tot[3];  // model_evals, eval calls, candidates
   int err_flag;
   int win_thread;
   int err_gpu;
@@ -482,8 +483,11 @@ k_plan(PlanParams P) {
       err->c = 0.0;
       P.gpu_count[s] = 0;
       if (P.stats) {
-        P.stats[2 * s] = (P.flags & IGP_F_STATS) ? 0 : -1;
-        P.stats[2 * s + 1] = (P.flags & IGP_F_STATS) ? 0 : -1;
+        const long long z = (P.flags & IGP_F_STATS) ? 0 : -1;
+        P.stats[4 * s] = z;
+        P.stats[4 * s + 1] = z;
+        P.stats[4 * s + 2] = z;
+        P.stats[4 * s + 3] = 0;
       }
     }
     return;
@@ -510,7 +514,9 @@ k_plan(PlanParams P) {
 
   Cand<MAXN> cd;
   int G = 0;
-  long long tot_evals = 0, tot_cands = 0;
+  // per-thread counters: committed totals and the current step's share
+  long long tot_evals = 0, tot_calls = 0, tot_cands = 0;
+  long long st_evals = 0, st_calls = 0, st_cands = 0;
   bool failed = false;
   ErrOut eo_fail;
   eo_fail.code = 0;
@@ -521,8 +527,6 @@ k_plan(PlanParams P) {
     const double ksch = ck[C_KSCH], nk = ck[C_NK];
     if (t == 0) {
       gs.best = NO_KEY;
-      gs.step_evals = 0;
-      gs.step_cands = 0;
       gs.err_flag = 0;
     }
     group_sync<GW>();
@@ -530,14 +534,14 @@ k_plan(PlanParams P) {
 
     auto process = [&](int j) {
       int n = 0, sum = 0;
-      long long ev = 0;
+      long long ev = 0, calls = 0;
       ErrOut eo;
       const double tsch_new = (ksch + delta_sch(hw, nres[j] + 1)) * nk;
-      int r = run_candidate<MAXN>(hw, sc, j, k, need, tsch_new, exact, &gs.best, cd, n, sum, ev, eo);
-      if (exact) {
-        atomicAdd(&gs.step_evals, (unsigned long long)ev);
-        atomicAdd(&gs.step_cands, 1u);
-      }
+      int r = run_candidate<MAXN>(hw, sc, j, k, need, tsch_new, exact, &gs.best, cd, n, sum, ev,
+                                  calls, eo);
+      st_evals += ev;
+      st_calls += calls;
+      st_cands += 1;
       if (r == R_ERROR) {
         atomicOr(&gs.err_flag, 1);
       } else if (r == R_FEAS) {
@@ -575,32 +579,30 @@ k_plan(PlanParams P) {
       // exact mode only: replay this step in the reference's candidate order
       // to find the first raising candidate and the PlanStats at that point.
       if (t == 0) {
-        long long ev_acc = 0;
-        int cands = 0;
         for (int j = 0; j < G; ++j) {
           if (occ[j] + need > cap) continue;
-          cands++;
+          tot_cands++;
           int n = 0, sum = 0;
-          long long ev = 0;
+          long long ev = 0, calls = 0;
           ErrOut eo;
           const double tsch_new = (ksch + delta_sch(hw, nres[j] + 1)) * nk;
-          int r = run_candidate<MAXN>(hw, sc, j, k, need, tsch_new, true, &gs.best, cd, n, sum, ev, eo);
-          ev_acc += ev;
+          int r = run_candidate<MAXN>(hw, sc, j, k, need, tsch_new, true, &gs.best, cd, n, sum, ev,
+                                      calls, eo);
+          tot_evals += ev;
+          tot_calls += calls;
           if (r == R_ERROR) {
             eo_fail = eo;
             break;
           }
         }
-        tot_evals += ev_acc;
-        tot_cands += cands;
       }
       failed = true;
       break;
     }
-    if (exact && t == 0) {
-      tot_evals += (long long)gs.step_evals;
-      tot_cands += gs.step_cands;
-    }
+    tot_evals += st_evals;
+    tot_calls += st_calls;
+    tot_cands += st_cands;
+    st_evals = st_calls = st_cands = 0;
     const unsigned long long bk = gs.best;
     if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
     group_sync<GW>();
@@ -651,6 +653,21 @@ k_plan(PlanParams P) {
     group_sync<GW>();
   }
 
+  // group totals of the counters
+  if (t == 0) gs.tot[0] = gs.tot[1] = gs.tot[2] = 0;
+  group_sync<GW>();
+  atomicAdd(&gs.tot[0], (unsigned long long)tot_evals);
+  atomicAdd(&gs.tot[1], (unsigned long long)tot_calls);
+  atomicAdd(&gs.tot[2], (unsigned long long)tot_cands);
+  group_sync<GW>();
+  if (t == 0 && P.stats) {
+    const bool st_ok = (P.flags & IGP_F_STATS) || failed;
+    P.stats[4 * s] = st_ok ? (long long)gs.tot[0] : -1;
+    P.stats[4 * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
+    P.stats[4 * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
+    P.stats[4 * s + 3] = (long long)gs.tot[1];
+  }
+
   if (failed) {
     if (t == 0) {
       err->code = eo_fail.code;
@@ -660,10 +677,6 @@ k_plan(PlanParams P) {
       err->b = eo_fail.b;
       err->c = eo_fail.c;
       P.gpu_count[s] = G;
-      if (P.stats) {
-        P.stats[2 * s] = tot_evals;
-        P.stats[2 * s + 1] = tot_cands;
-      }
     }
     return;
   }
@@ -769,10 +782,6 @@ k_plan(PlanParams P) {
       err->a = err->b = err->c = 0.0;
     }
     P.gpu_count[s] = G;
-    if (P.stats) {
-      P.stats[2 * s] = (P.flags & IGP_F_STATS) ? tot_evals : -1;
-      P.stats[2 * s + 1] = (P.flags & IGP_F_STATS) ? tot_cands : -1;
-    }
   }
 }
 
@@ -1011,11 +1020,12 @@ size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, 
   return ws_layout(n_scen, m, h.cap, flags).total;
 }
 
-int igp_plan_batch_device(const double *wl, int n_scen, int m, const double *hw_h, int b_max,
-                          const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
-                          int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
-                          double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
-                          void *workspace, size_t workspace_bytes, int flags, void *stream) {
+static int plan_device_impl(const double *wl, int n_scen, int m, const double *hw_h, int b_max,
+                            const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
+                            int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,
+                            double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
+                            void *workspace, size_t workspace_bytes, int flags, void *stream,
+                            int stages) {
   if (n_scen < 0 || m < 0 || !hw_h) return IGP_E_ARG;
   if (n_scen == 0) return IGP_E_OK;
   Hw hw = make_hw(hw_h, b_max);
@@ -1055,20 +1065,37 @@ int igp_plan_batch_device(const double *wl, int n_scen, int m, const double *hw_
   P.gpu_count = gpu_count;
   P.stats = stats;
   P.err = err;
-  CK(cudaMemsetAsync(P.risky, 0, (size_t)n_scen * 4, st));
-  k_fill_int<<<nblk(n_scen, 256), 256, 0, st>>>(P.perr, n_scen, INT_MAX);
-  if (m > 0) {
-    long long tot = (long long)n_scen * m;
-    k_prologue_plan<<<nblk(tot, 256), 256, 0, st>>>(P);
-    k_sort<<<nblk(n_scen, 4), 128, 0, st>>>(P);
-    k_build<<<nblk(tot, 256), 256, 0, st>>>(P);
+  if (stages & 1) {
+    CK(cudaMemsetAsync(P.risky, 0, (size_t)n_scen * 4, st));
+    k_fill_int<<<nblk(n_scen, 256), 256, 0, st>>>(P.perr, n_scen, INT_MAX);
+    if (m > 0) {
+      long long tot = (long long)n_scen * m;
+      k_prologue_plan<<<nblk(tot, 256), 256, 0, st>>>(P);
+      k_sort<<<nblk(n_scen, 4), 128, 0, st>>>(P);
+      k_build<<<nblk(tot, 256), 256, 0, st>>>(P);
+    }
   }
-  if (hw.cap <= 48) launch_plan<48>(P, st);
-  else if (hw.cap <= 128) launch_plan<128>(P, st);
-  else launch_plan<256>(P, st);
+  if (stages & 2) {
+    if (hw.cap <= 48) launch_plan<48>(P, st);
+    else if (hw.cap <= 128) launch_plan<128>(P, st);
+    else launch_plan<256>(P, st);
+  }
   CK(cudaGetLastError());
   return IGP_E_OK;
 }
+
+#define PLAN_ARGS_DECL                                                                          \
+  const double *wl, int n_scen, int m, const double *hw_h, int b_max, const int32_t *name_rank, \
+      int rank_stride, int32_t *gpu_of, int32_t *pos, int32_t *units, int32_t *batch,           \
+      int32_t *lb, double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,             \
+      void *workspace, size_t workspace_bytes, int flags, void *stream
+#define PLAN_ARGS_PASS                                                                        \
+  wl, n_scen, m, hw_h, b_max, name_rank, rank_stride, gpu_of, pos, units, batch, lb, pred,     \
+      gpu_count, stats, err, workspace, workspace_bytes, flags, stream
+
+int igp_plan_batch_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PASS, 3); }
+int igp_plan_prepare_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PASS, 1); }
+int igp_plan_place_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PASS, 2); }
 
 int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h, int b_max,
                         const int32_t *name_rank, int rank_stride, int32_t *gpu_of, int32_t *pos,
@@ -1090,7 +1117,7 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
   size_t o_i32 = off; off = align_up(off + Sm * 4 * 5);
   size_t o_pred = off; off = align_up(off + (pred ? Sm * 80 : 0));
   size_t o_gc = off; off = align_up(off + (size_t)n_scen * 4);
-  size_t o_st = off; off = align_up(off + (size_t)n_scen * 16);
+  size_t o_st = off; off = align_up(off + (size_t)n_scen * 32);
   size_t o_err = off; off = align_up(off + (size_t)n_scen * sizeof(igp_error));
   if (!workspace || workspace_bytes < off) return IGP_E_ARG;
   char *ws = (char *)workspace;
@@ -1120,7 +1147,7 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
     if (pred) CK(cudaMemcpyAsync(pred, d_pred, Sm * 80, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(gpu_count, d_gc, (size_t)n_scen * 4, cudaMemcpyDeviceToHost, st));
-  if (stats) CK(cudaMemcpyAsync(stats, d_st, (size_t)n_scen * 16, cudaMemcpyDeviceToHost, st));
+  if (stats) CK(cudaMemcpyAsync(stats, d_st, (size_t)n_scen * 32, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(err, d_err, (size_t)n_scen * sizeof(igp_error), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int s = 0; s < n_scen; ++s)
