@@ -81,10 +81,23 @@ def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
     return int(lib.igp_plan_workspace_bytes(S, m, _np_ptr(h), b_max, flags))
 
 
+POOL_RETRY = 12  # 8*G + 4*m <= 12*m records always suffice (csrc/place.cuh)
+
+
 def plan_device(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True):
     """Plan S scenarios; wl is [S,16,m] (or [16,m]) float64, rank [m] or [S,m].
 
-    Returns numpy arrays (all per scenario, input order)."""
+    Returns numpy arrays (all per scenario, input order).  A scenario whose
+    tiles outgrow the default record pool (IGP_E_CAPACITY) is re-planned with
+    the pool size that is sufficient for any plan."""
+    res = _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred)
+    if (res["err"]["code"] == 7).any() and ((flags >> 8) & 0xFF) < POOL_RETRY:
+        res = _plan_device_once(wl, hw_vec, b_max, rank, (flags & ~0xFF00) | (POOL_RETRY << 8),
+                                device, want_pred)
+    return res
+
+
+def _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred):
     torch = _torch()
     lib = _native.lib_for_compute()
     device = _dev(device)

@@ -15,9 +15,9 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 LIB_DIR = os.path.join(PKG, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libigniter_b200.so")
+LIB_PATH = os.environ.get("IGP_LIB") or os.path.join(LIB_DIR, "libigniter_b200.so")
 SOURCES = [os.path.join(PKG, "csrc", "igniter_kernels.cu")]
-DEPS = SOURCES + [os.path.join(PKG, "csrc", "exact_fp64.cuh"),
+DEPS = SOURCES + [os.path.join(PKG, "csrc", "exact_fp64.cuh"), os.path.join(PKG, "csrc", "place.cuh"),
                   os.path.join(REPO, "include", "igniter_b200.h")]
 
 NVCC_FLAGS = [

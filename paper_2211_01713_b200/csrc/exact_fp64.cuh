@@ -18,6 +18,7 @@ struct Hw {
   double pmax, fmax, pidle, bw, af, asch, bsch, runit, rmax, price, fminfrac;
   double fmin;  // f_min_mhz = f_min_frac * freq_max_mhz  (model.py:108-110)
   int cap;      // max_units = int(round(r_max / r_unit)) (planner.py:72-73)
+  int margin_ok;  // scale = f / fmax is finite and > 0 for every reachable f
   int b_max;
 };
 

@@ -1,0 +1,1000 @@
+// place.cuh -- the greedy placement (Alg. 1 + Alg. 2) on the device.
+//
+// Restates planner.py:258-325 (plan), :133-162 (_alloc_units), :218-246
+// (_build_plan) and model.py:273-317 (_eval_entries) for S independent
+// scenarios.  Included by igniter_kernels.cu (needs prologue_one,
+// entry_consts, make_hw from there).
+//
+// Device layout, per scenario (all in the caller's workspace):
+//   per workload, in placement order k (sorted by (-lb, name)):
+//     cold[k][12]   constants for unit changes (gamma, k4, k5, batch, alpha/beta
+//                   of power and cache, k_sch, n_kernels, lb, input index)
+//     nw[k][8]      k's check record at its lower bound (the newcomer's state)
+//     tbl[k][16][4] solo (k_act, power, cache, error) at u = lb .. lb+15: a
+//                   unit bump is one 32-byte lookup instead of two divisions
+//   per open GPU j:
+//     gstate[j]     occupied units | residents << 16 (the prefilter scans this)
+//     goff/gcap[j]  its tile in the record pool
+//     gfold[j][4]   Neumaier (s, c) of the power and cache sums over residents
+//   record pool (tiles; a GPU's residents are contiguous, in placement order):
+//     rec[r][8]     64-byte check record: k_act, cache, t_sch for the next
+//                   candidate size, alpha_cache, t_load, t_feedback, t_half, power
+//     frec[r][2]    (power, cache) -- the fold stream
+//     pfx[r][4]     Neumaier states of both sums BEFORE this resident
+//     meta[r]       workload k, units, lower bound
+//   Tiles start with 4 records and double on overflow (copied); the pool holds
+//   pool_factor * m records, enough for every realistic plan (E_CAPACITY
+//   otherwise, and the host retries with a larger pool).
+#pragma once
+
+namespace igp {
+
+constexpr int TB = 16;     // solo-table entries per workload
+constexpr int TILE0 = 4;   // initial tile capacity
+enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_NF };
+enum { SF_RISKY = 1, SF_NO_MARGIN = 2 };
+enum { R_FEAS = 0, R_INFEAS = 1, R_PRUNED = 2, R_ERROR = 3 };
+
+struct Meta {
+  int32_t k;
+  uint16_t u;
+  uint16_t lb;
+};
+
+struct WsLayout {
+  size_t by_rank, order, cold, nw, tbl, gstate, goff, gcap, gfold, rec, frec, pfx, meta,
+      lane_units, sflags, perr, sched, total;
+  int lanes;
+  long long pool_recs;  // records per scenario
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int pool_factor(int flags) {
+  const int f = (flags >> 8) & 0xff;
+  return f ? f : 6;
+}
+
+static WsLayout ws_layout(int S, int m, int cap, int flags) {
+  WsLayout L;
+  size_t off = 0;
+  const size_t mm = (size_t)(m > 0 ? m : 1);
+  const size_t Sm = (size_t)S * mm;
+  const int capx = cap > 0 ? cap : 1;
+  L.lanes = (flags & IGP_F_CTA) ? 256 : 32;
+  L.pool_recs = (long long)pool_factor(flags) * (long long)mm + 4 * TILE0;
+  const size_t Sp = (size_t)S * (size_t)L.pool_recs;
+  L.by_rank = off; off = align_up(off + Sm * 4);
+  L.order = off; off = align_up(off + Sm * 4);
+  L.cold = off; off = align_up(off + Sm * C_NF * 8);
+  L.nw = off; off = align_up(off + Sm * R_NF * 8);
+  L.tbl = off; off = align_up(off + Sm * TB * 4 * 8);
+  L.gstate = off; off = align_up(off + Sm * 4);
+  L.goff = off; off = align_up(off + Sm * 4);
+  L.gcap = off; off = align_up(off + Sm * 4);
+  L.gfold = off; off = align_up(off + Sm * 4 * 8);
+  L.rec = off; off = align_up(off + Sp * R_NF * 8);
+  L.frec = off; off = align_up(off + Sp * 2 * 8);
+  L.pfx = off; off = align_up(off + Sp * 4 * 8);
+  L.meta = off; off = align_up(off + Sp * sizeof(Meta));
+  L.lane_units = off; off = align_up(off + (size_t)S * L.lanes * capx * 2);
+  L.sflags = off; off = align_up(off + (size_t)S * 4);
+  L.perr = off; off = align_up(off + (size_t)S * 4);
+  L.sched = off; off = align_up(off + 4);
+  L.total = off;
+  return L;
+}
+
+struct PlanParams {
+  Hw hw;
+  int S, m, flags;
+  const double *wl;     // [S][16][m]
+  const int32_t *rank;  // name ranks
+  int rank_stride;
+  int lanes;
+  long long pool_recs;
+  // workspace
+  int32_t *by_rank, *order, *sflags, *perr, *goff, *gcap;
+  int32_t *sched;  // persistent-kernel scenario counter (zeroed before each launch)
+  uint32_t *gstate;
+  double *cold, *nw, *tbl, *gfold, *rec, *frec, *pfx;
+  Meta *meta;
+  uint16_t *lane_units;
+  // outputs
+  int32_t *gpu_of, *pos, *units, *batch, *lb, *gpu_count;
+  double *pred;
+  int64_t *stats;
+  igp_error *err;
+};
+
+// ---------------------------------------------------------------------------
+// prepare stage
+// ---------------------------------------------------------------------------
+// thread per (scenario, workload): batch, lb, first-error key, risk flags, by_rank
+__global__ void k_prologue_plan(PlanParams P) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)P.S * P.m) return;
+  const int s = (int)(gid / P.m), i = (int)(gid % P.m);
+  const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
+  int b = -1, u = -1;
+  double opnd;
+  const int rc = prologue_one(wl, P.m, i, P.hw, nullptr, b, u, opnd);
+  const size_t o = (size_t)s * P.m + i;
+  P.batch[o] = b;
+  P.lb[o] = u;
+  const int32_t *rk = P.rank + (size_t)s * P.rank_stride;
+  P.by_rank[(size_t)s * P.m + rk[i]] = i;
+  if (rc) {
+    atomicMin(&P.perr[s], i);  // first error in INPUT order (planner.py:280-282)
+    return;
+  }
+  // NonPositiveDenominatorError screen: denom(u) = u*r_unit + k4 is
+  // non-decreasing in u and k_act(u) = gamma/denom(u) + k5 is monotone in u
+  // (direction = sign of gamma) under round-to-nearest, so the two ends of the
+  // reachable range [lb, cap] decide whether any evaluation can raise.
+  double cold[C_NF], slot[S_NF];
+  entry_consts(wl, P.m, i, b, P.hw, cold, slot);
+  const Solo a = solo_from_cold(cold, (double)u * P.hw.runit);
+  const Solo c = solo_from_cold(cold, (double)P.hw.cap * P.hw.runit);
+  int fl = (a.err || c.err) ? SF_RISKY : 0;
+  // The margin test needs every t_inf term non-negative and finite
+  // (validated by WorkloadSpec/Coefficients; raw C-ABI callers might not be).
+  if (!(slot[S_TLOAD] >= 0.0) || !(slot[S_TFB] >= 0.0) || !(cold[C_KSCH] >= 0.0) ||
+      !(cold[C_NK] >= 0.0) || !(slot[S_ACACHE] >= 0.0) || !(slot[S_ACACHE] <= 1e6) ||
+      !isfinite(slot[S_TLOAD] + slot[S_TFB] + slot[S_THALF] + cold[C_KSCH] * cold[C_NK]))
+    fl |= SF_NO_MARGIN;
+  if (!(u <= 0xffff)) fl |= SF_RISKY;
+  if (fl) atomicOr(&P.sflags[s], fl);
+}
+
+// warp per scenario: stable counting sort by (-lb, name rank) (planner.py:284)
+__global__ void k_sort(PlanParams P) {
+  __shared__ int hist[4][257];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int s = blockIdx.x * 4 + w;
+  if (s >= P.S) return;
+  if (P.perr[s] != INT_MAX) return;
+  const int cap = P.hw.cap, m = P.m;
+  const int32_t *lb = P.lb + (size_t)s * m;
+  const int32_t *byr = P.by_rank + (size_t)s * m;
+  int32_t *order = P.order + (size_t)s * m;
+  int *h = hist[w];
+  for (int b = lane; b <= cap; b += 32) h[b] = 0;
+  __syncwarp();
+  for (int i = lane; i < m; i += 32) atomicAdd(&h[cap - lb[i]], 1);
+  __syncwarp();
+  if (lane == 0) {
+    int acc = 0;
+    for (int b = 0; b < cap; ++b) {
+      const int c = h[b];
+      h[b] = acc;
+      acc += c;
+    }
+  }
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < m; base += 32) {
+    const int r = base + lane;
+    const bool act = r < m;
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    if (act) {
+      const int i = byr[r];
+      const int key = cap - lb[i];
+      const unsigned peers = __match_any_sync(am, key);
+      const int before = __popc(peers & lt);
+      order[h[key] + before] = i;
+      __syncwarp(am);
+      if (before == 0) h[key] += __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// thread per (scenario, placement position k): cold constants + newcomer record
+__global__ void k_build(PlanParams P) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)P.S * P.m) return;
+  const int s = (int)(gid / P.m), k = (int)(gid % P.m);
+  if (P.perr[s] != INT_MAX) return;
+  const size_t sm = (size_t)s * P.m;
+  const int i = P.order[sm + k];
+  const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
+  double cold[C_NF], slot[S_NF];
+  const int b = P.batch[sm + i], u = P.lb[sm + i];
+  entry_consts(wl, P.m, i, b, P.hw, cold, slot);
+  cold[C_LB] = (double)u;
+  cold[C_WIN] = (double)i;
+  const Solo so = solo_from_cold(cold, (double)u * P.hw.runit);
+  double *cd = P.cold + (sm + k) * C_NF;
+#pragma unroll
+  for (int f = 0; f < C_NF; ++f) cd[f] = cold[f];
+  double *nw = P.nw + (sm + k) * R_NF;
+  nw[R_KA] = so.ka;
+  nw[R_CA] = so.ca;
+  nw[R_TSN] = (double)so.err;  // the newcomer's solo error code at lb
+  nw[R_ACACHE] = slot[S_ACACHE];
+  nw[R_TLOAD] = slot[S_TLOAD];
+  nw[R_TFB] = slot[S_TFB];
+  nw[R_THALF] = slot[S_THALF];
+  nw[R_PW] = so.pw;
+}
+
+// thread per (scenario, k, v): solo table entry at u = lb + v (model.py:285-297)
+__global__ void k_table(PlanParams P) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)P.S * P.m * TB) return;
+  const long long sk = gid / TB;
+  const int v = (int)(gid % TB);
+  const int s = (int)(sk / P.m);
+  if (P.perr[s] != INT_MAX) return;
+  const double *cd = P.cold + sk * C_NF;
+  const int u = (int)cd[C_LB] + v;
+  double *t = P.tbl + gid * 4;
+  if (u > P.hw.cap) {
+    t[0] = t[1] = t[2] = t[3] = 0.0;
+    return;
+  }
+  const Solo so = solo_from_cold(cd, (double)u * P.hw.runit);
+  t[0] = so.ka;
+  t[1] = so.pw;
+  t[2] = so.ca;
+  t[3] = (double)so.err;
+}
+
+// ---------------------------------------------------------------------------
+// place stage
+// ---------------------------------------------------------------------------
+struct GroupSmem {
+  unsigned long long best;
+  unsigned long long tot[3];  // model_evals, eval calls, candidates
+  int err_flag;
+  int win_thread;
+  int err_gpu;
+  int pool_top;
+  int abort_code;
+  int next;  // persistent scheduling: the scenario this group plans next
+};
+
+template <int GW>
+__device__ __forceinline__ void group_sync() {
+  if (GW == 1) __syncwarp();
+  else __syncthreads();
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ Solo solo_lookup(const double *tbl, const double *cold, const Hw &hw,
+                                            int k, int lb, int u) {
+  const int v = u - lb;
+  if (v >= 0 && v < TB) {
+    const double *t = tbl + ((size_t)k * TB + v) * 4;
+    Solo so;
+    so.ka = t[0];
+    so.pw = t[1];
+    so.ca = t[2];
+    so.err = (int)t[3];
+    return so;
+  }
+  return solo_from_cold(cold + (size_t)k * C_NF, (double)u * hw.runit);
+}
+
+struct ErrOut {
+  int code, k;
+  double a, b, c;
+};
+
+__device__ __forceinline__ void err_operands(const Hw &hw, const double *ce, int u, int code,
+                                             ErrOut &eo) {
+  const double r = (double)u * hw.runit;
+  const double denom = r + ce[C_K4];
+  eo.code = code;
+  if (code == IGP_E_DENOM) {
+    eo.a = denom;
+    eo.b = r;
+    eo.c = ce[C_K4];
+  } else {
+    eo.a = ce[C_GAMMA] / denom + ce[C_K5];
+    eo.b = ce[C_BATCH];
+    eo.c = r;
+  }
+}
+
+// Modified-resident bitmask of a candidate (positions < MAXN).
+template <int MAXN>
+struct ModMask {
+  static constexpr int W = (MAXN + 63) / 64;
+  unsigned long long w[W];
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int i = 0; i < W; ++i) w[i] = 0ull;
+  }
+  __device__ __forceinline__ bool test(int i) const {
+    unsigned long long x = w[0];
+#pragma unroll
+    for (int q = 1; q < W; ++q)
+      if ((i >> 6) == q) x = w[q];
+    return (x >> (i & 63)) & 1ull;
+  }
+  __device__ __forceinline__ void set(int i) {
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if ((i >> 6) == q) w[q] |= 1ull << (i & 63);
+  }
+};
+
+template <int MAXN>
+struct LaneArrays {  // values of residents bumped inside the current candidate
+  int u[MAXN];
+  double ka[MAXN], pw[MAXN], ca[MAXN];
+};
+
+// One scenario per group of GW warps (GW == 1: four scenarios per 128-thread
+// CTA; GW > 1: one scenario per CTA).
+template <int MAXN, int GW>
+__global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32, GW == 1 ? IGP_MINB_WARP : 1)
+k_place(PlanParams P) {
+  constexpr int GT = GW * 32;
+  constexpr int GPB = (GW == 1) ? 4 : 1;
+  constexpr unsigned long long NO_KEY = ~0ull;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ GroupSmem gsm[GPB];
+  __shared__ int qsm[GPB * GW][64];
+  const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
+  GroupSmem &gs = gsm[grp];
+  // Persistent groups: each pulls the next scenario when it finishes one, so
+  // scenarios of unequal length do not leave SMs idle at the end.
+  for (;;) {
+  if (t == 0) gs.next = atomicAdd(P.sched, 1);
+  group_sync<GW>();
+  const int s = gs.next;
+  group_sync<GW>();
+  if (s >= P.S) break;
+  int *q = qsm[grp * GW + wi];
+  const Hw &hw = P.hw;
+  const int m = P.m, cap = hw.cap;
+  const size_t sm = (size_t)s * m;
+  igp_error *err = P.err + s;
+
+  if (P.perr[s] != INT_MAX) {  // prologue error, input order (planner.py:280-282)
+    if (t == 0) {
+      const int i = P.perr[s];
+      int b, u;
+      double opnd = 0.0;
+      const double *wl = P.wl + (size_t)s * IGP_WL_NF * m;
+      const int rc = prologue_one(wl, m, i, hw, nullptr, b, u, opnd);
+      err->code = rc;
+      err->workload = i;
+      err->gpu = -1;
+      err->a = opnd;
+      err->b = (double)hw.b_max;
+      err->c = 0.0;
+      P.gpu_count[s] = 0;
+      if (P.stats) {
+        const long long z = (P.flags & IGP_F_STATS) ? 0 : -1;
+        P.stats[4 * s] = z;
+        P.stats[4 * s + 1] = z;
+        P.stats[4 * s + 2] = z;
+        P.stats[4 * s + 3] = 0;
+      }
+    }
+    continue;
+  }
+
+  const double *cold = P.cold + sm * C_NF;
+  const double *nwt = P.nw + sm * R_NF;
+  const double *tbl = P.tbl + sm * TB * 4;
+  uint32_t *gstate = P.gstate + sm;
+  int32_t *goff = P.goff + sm;
+  int32_t *gcap = P.gcap + sm;
+  double *gfold = P.gfold + sm * 4;
+  const size_t sp = (size_t)s * (size_t)P.pool_recs;
+  double *rec = P.rec + sp * R_NF;
+  double *frec = P.frec + sp * 2;
+  double *pfx = P.pfx + sp * 4;
+  Meta *meta = P.meta + sp;
+  uint16_t *lane_units = P.lane_units + (size_t)s * P.lanes * cap;
+  const int sflags = P.sflags[s];
+  const bool exact = (P.flags & IGP_F_STATS) || (sflags & SF_RISKY);
+  const bool margin = !(sflags & SF_NO_MARGIN) && hw.margin_ok;
+  const unsigned lt = (1u << lane) - 1u;
+
+  LaneArrays<MAXN> L;
+  ModMask<MAXN> mod;
+  int G = 0;
+  long long tot_evals = 0, tot_calls = 0, tot_cands = 0;
+  long long st_evals = 0, st_calls = 0, st_cands = 0;
+  int fail_code = 0;
+  ErrOut eo_fail;
+  eo_fail.code = 0;
+  eo_fail.k = -1;
+  if (t == 0) {
+    gs.pool_top = 0;
+    gs.abort_code = 0;
+  }
+
+  for (int k = 0; k < m; ++k) {
+    // the newcomer (planner.py:291-292)
+    const double *ck = cold + (size_t)k * C_NF;
+    const double *nk_rec = nwt + (size_t)k * R_NF;
+    const int need = (int)ck[C_LB];
+    const double ksch = ck[C_KSCH], nkern = ck[C_NK];
+    const double nw_ka = nk_rec[R_KA], nw_ca = nk_rec[R_CA], nw_pw = nk_rec[R_PW];
+    const double nw_acache = nk_rec[R_ACACHE], nw_tload = nk_rec[R_TLOAD];
+    const double nw_tfb = nk_rec[R_TFB], nw_thalf = nk_rec[R_THALF];
+    const int nw_err = (int)nk_rec[R_TSN];
+    if (t == 0) {
+      gs.best = NO_KEY;
+      gs.err_flag = 0;
+    }
+    group_sync<GW>();
+    unsigned long long my_best = NO_KEY;
+
+    // ---- the step's candidates: per-lane state machine with dynamic refill ----
+    // A lane owns at most one candidate GPU.  One loop iteration advances every
+    // busy lane by one resident check of Alg. 2 (planner.py:152-161), plus the
+    // evaluation it needs first and the unit bump it may cause.  Idle lanes
+    // are refilled from a per-warp ring queue fed by a coalesced prefilter
+    // scan (planner.py:297-299), in ascending j, so early (low-j, low-inter)
+    // keys prune later candidates and lanes never wait for a round's longest
+    // candidate.  serial != 0 replays the step in the reference's order on
+    // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
+    auto run_step = [&](const bool serial) {
+      int qhead = 0, qtail = 0;
+      int scan = serial ? 0 : wi * 32;
+      const int scan_stride = serial ? 32 : GT;
+      const unsigned take_mask = serial ? 1u : FULL;
+      int cj = -1, c_nres = 0, c_occ = 0, c_sum = 0, c_i = 0, c_dirty = 0, c_off = 0;
+      int c_pend = -1, c_pcode = 0, c_nu = 0;
+      bool c_flag = false, c_need = false;
+      double c_C = 0.0, c_scale = 1.0, c_inv = 1.0, c_tsn = 0.0;
+      double c_nka = 0.0, c_npw = 0.0, c_nca = 0.0;
+      bool stop = false;
+
+      auto finish = [&](int result) {
+        if (result == R_ERROR) {
+          atomicOr(&gs.err_flag, 1);
+          if (serial) {
+            int ek, eu;
+            if (c_pend == c_nres) {
+              ek = k;
+              eu = c_nu;
+            } else {
+              const Meta mt = meta[c_off + c_pend];
+              ek = mt.k;
+              eu = mod.test(c_pend) ? L.u[c_pend] : (int)mt.u;
+            }
+            err_operands(hw, cold + (size_t)ek * C_NF, eu, c_pcode, eo_fail);
+            eo_fail.k = ek;
+            stop = true;
+          }
+        } else if (result == R_FEAS) {
+          const unsigned long long key =
+              ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
+          if (key < my_best) {
+            my_best = key;
+            uint16_t *lu = lane_units + (size_t)t * cap;
+            for (int qq = 0; qq < c_nres; ++qq)
+              lu[qq] = mod.test(qq) ? (uint16_t)L.u[qq] : meta[c_off + qq].u;
+            lu[c_nres] = (uint16_t)c_nu;
+          }
+          atomicMin(&gs.best, key);
+        }
+        cj = -1;
+      };
+
+      while (true) {
+        // warp-uniform stop (set by the serial replay's first raising candidate)
+        if (__any_sync(FULL, stop)) break;
+        const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
+        if (idle) {
+          const int nidle = __popc(idle);
+          while (qtail - qhead < nidle && scan < G) {
+            const int jj = scan + lane;
+            const bool pass = (jj < G) && ((int)(gstate[jj] & 0xffffu) + need <= cap);
+            const unsigned mask = __ballot_sync(FULL, pass);
+            if (pass) q[(qtail + __popc(mask & lt)) & 63] = jj;
+            qtail += __popc(mask);
+            scan += scan_stride;
+          }
+          __syncwarp();
+          if ((idle >> lane) & 1u) {
+            const int r = __popc(idle & lt);
+            if (qhead + r < qtail) {
+              const int j = q[(qhead + r) & 63];
+              st_cands += 1;
+              const volatile unsigned long long *bp = &gs.best;
+              if (exact || ((((unsigned long long)need) << 32) | (unsigned)j) <= *bp) {
+                // residents_j + [newcomer] (planner.py:302-304)
+                const uint32_t g = gstate[j];
+                cj = j;
+                c_occ = (int)(g & 0xffffu);
+                c_nres = (int)(g >> 16);
+                c_off = goff[j];
+                c_sum = c_occ + need;
+                c_i = 0;
+                c_dirty = c_nres;
+                c_flag = false;
+                c_need = true;
+                c_nu = need;
+                c_nka = nw_ka;
+                c_npw = nw_pw;
+                c_nca = nw_ca;
+                c_tsn = (ksch + delta_sch(hw, c_nres + 1)) * nkern;
+                mod.clear();
+                c_pend = -1;
+                if (exact) {
+                  for (int qq = 0; qq < c_nres && c_pend < 0; ++qq) {
+                    const Meta mt = meta[c_off + qq];
+                    const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, mt.u);
+                    if (so.err) {
+                      c_pend = qq;
+                      c_pcode = so.err;
+                    }
+                  }
+                  if (c_pend < 0 && nw_err) {
+                    c_pend = c_nres;
+                    c_pcode = nw_err;
+                  }
+                }
+              }
+            }
+          }
+          qhead = min(qtail, qhead + nidle);
+          __syncwarp();
+        }
+        const unsigned busy = __ballot_sync(FULL, cj >= 0);
+        if (!busy) {
+          if (qhead >= qtail && scan >= G) break;
+          continue;
+        }
+        if (cj < 0) continue;
+        if (c_need) {
+          if (c_pend >= 0) {
+            finish(R_ERROR);
+            continue;
+          }
+          // _eval_entries device terms (model.py:299-305), folded in resident
+          // order from the last valid cached prefix state
+          const double *stp = (c_dirty == c_nres) ? gfold + (size_t)cj * 4
+                                                  : pfx + (size_t)(c_off + c_dirty) * 4;
+          Neumaier fp, fc;
+          fp.s = stp[0];
+          fp.c = stp[1];
+          fc.s = stp[2];
+          fc.c = stp[3];
+          for (int qq = c_dirty; qq < c_nres; ++qq) {
+            double pw, ca;
+            if (mod.test(qq)) {
+              pw = L.pw[qq];
+              ca = L.ca[qq];
+            } else {
+              const double2 f2 = *reinterpret_cast<const double2 *>(frec + (size_t)(c_off + qq) * 2);
+              pw = f2.x;
+              ca = f2.y;
+            }
+            fp.add(pw);
+            fc.add(ca);
+          }
+          fp.add(c_npw);
+          fc.add(c_nca);
+          const double f = frequency(hw, hw.pidle + fp.result());
+          c_C = fc.result();
+          c_scale = f / hw.fmax;
+          c_inv = (c_scale == 1.0) ? 1.0 : 1.0 / c_scale;
+          st_evals += c_nres + 1;
+          st_calls += 1;
+          c_need = false;
+        }
+        // check resident c_i: t_inf > t_half (model.py:308-313, planner.py:158)
+        {
+          const int i = c_i;
+          double ka, ca, t_sch, acache, t_load, t_fb, t_half;
+          if (i == c_nres) {
+            ka = c_nka;
+            ca = c_nca;
+            t_sch = c_tsn;
+            acache = nw_acache;
+            t_load = nw_tload;
+            t_fb = nw_tfb;
+            t_half = nw_thalf;
+          } else {
+            const double *r = rec + (size_t)(c_off + i) * R_NF;
+            const double2 kc = *reinterpret_cast<const double2 *>(r + R_KA);
+            const double2 ta = *reinterpret_cast<const double2 *>(r + R_TSN);
+            const double2 lf = *reinterpret_cast<const double2 *>(r + R_TLOAD);
+            t_half = r[R_THALF];
+            t_sch = ta.x;
+            acache = ta.y;
+            t_load = lf.x;
+            t_fb = lf.y;
+            if (mod.test(i)) {
+              ka = L.ka[i];
+              ca = L.ca[i];
+            } else {
+              ka = kc.x;
+              ca = kc.y;
+            }
+          }
+          const double x = t_sch + ka * (1.0 + acache * (c_C - ca));
+          double t_gpu = x;  // x / 1.0 == x exactly
+          if (c_scale != 1.0) {
+            t_gpu = x * c_inv;
+            if (margin) {
+              const double tq = (t_load + t_gpu) + t_fb;
+              if (!(fabs(tq - t_half) > tq * 0x1p-48 + 0x1p-1000)) t_gpu = x / c_scale;
+            } else {
+              t_gpu = x / c_scale;
+            }
+          }
+          const double t_inf = (t_load + t_gpu) + t_fb;
+          if (t_inf > t_half) {
+            c_sum += 1;
+            if (!exact) {
+              // units only grow: an overflow or a key that already loses ends
+              // the candidate before any further work
+              if (c_sum > cap) {
+                finish(R_INFEAS);
+                continue;
+              }
+              const volatile unsigned long long *bp = &gs.best;
+              const unsigned long long key =
+                  ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
+              if (key > *bp) {
+                finish(R_PRUNED);
+                continue;
+              }
+            }
+            Solo so;
+            if (i == c_nres) {
+              c_nu += 1;
+              so = solo_lookup(tbl, cold, hw, k, need, c_nu);
+              c_nka = so.ka;
+              c_npw = so.pw;
+              c_nca = so.ca;
+            } else {
+              const Meta mt = meta[c_off + i];
+              const int u = (mod.test(i) ? L.u[i] : (int)mt.u) + 1;
+              so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
+              L.u[i] = u;
+              L.ka[i] = so.ka;
+              L.pw[i] = so.pw;
+              L.ca[i] = so.ca;
+              mod.set(i);
+            }
+            if (i < c_dirty) c_dirty = i;
+            if (exact && so.err && c_pend < 0) {
+              c_pend = i;
+              c_pcode = so.err;
+            }
+            c_flag = true;
+            c_need = true;
+          }
+        }
+        c_i += 1;
+        if (c_i > c_nres) {
+          if (c_flag && c_sum <= cap) {
+            c_i = 0;
+            c_flag = false;
+            // The reference re-evaluates at every pass start (rows = None,
+            // planner.py:151); if nothing changed since the last evaluation the
+            // values are identical, so only exact PlanStats account for it.
+            if (exact && !c_need) {
+              st_evals += c_nres + 1;
+              st_calls += 1;
+            }
+          } else {
+            finish(c_sum <= cap ? R_FEAS : R_INFEAS);
+          }
+        }
+      }
+    };
+
+    run_step(false);
+    group_sync<GW>();
+
+    if (gs.err_flag) {
+      // exact mode only: replay the step in the reference's candidate order to
+      // find the first raising candidate and the PlanStats at that point
+      st_evals = st_calls = st_cands = 0;
+      if (wi == 0) run_step(true);
+      if (t != 0) st_evals = st_calls = st_cands = 0;
+      tot_evals += st_evals;
+      tot_calls += st_calls;
+      tot_cands += st_cands;
+      fail_code = 1;
+      break;
+    }
+    tot_evals += st_evals;
+    tot_calls += st_calls;
+    tot_cands += st_cands;
+    st_evals = st_calls = st_cands = 0;
+    const unsigned long long bk = gs.best;
+    if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
+    group_sync<GW>();
+
+    // ---- commit (planner.py:312-319), warp 0 of the group ----
+    if (wi == 0) {
+      if (bk == NO_KEY) {
+        if (lane == 0) {
+          const int off = gs.pool_top;
+          if (off + TILE0 > P.pool_recs) {
+            gs.abort_code = IGP_E_CAPACITY;
+          } else {
+            gs.pool_top = off + TILE0;
+            goff[G] = off;
+            gcap[G] = TILE0;
+            gstate[G] = (uint32_t)need | (1u << 16);
+            double *r = rec + (size_t)off * R_NF;
+            r[R_KA] = nw_ka;
+            r[R_CA] = nw_ca;
+            r[R_TSN] = (ksch + delta_sch(hw, 2)) * nkern;
+            r[R_ACACHE] = nw_acache;
+            r[R_TLOAD] = nw_tload;
+            r[R_TFB] = nw_tfb;
+            r[R_THALF] = nw_thalf;
+            r[R_PW] = nw_pw;
+            frec[(size_t)off * 2] = nw_pw;
+            frec[(size_t)off * 2 + 1] = nw_ca;
+            double *pp = pfx + (size_t)off * 4;
+            pp[0] = pp[1] = pp[2] = pp[3] = 0.0;
+            meta[off] = Meta{k, (uint16_t)need, (uint16_t)need};
+            Neumaier fp, fc;
+            fp.first(nw_pw);
+            fc.first(nw_ca);
+            double *gf = gfold + (size_t)G * 4;
+            gf[0] = fp.s;
+            gf[1] = fp.c;
+            gf[2] = fc.s;
+            gf[3] = fc.c;
+          }
+        }
+      } else {
+        const int j = (int)(bk & 0xffffffffu);
+        const uint16_t *lu = lane_units + (size_t)gs.win_thread * cap;
+        const int nres = (int)(gstate[j] >> 16);
+        const int n = nres + 1;
+        int off = goff[j];
+        const int tcap = gcap[j];
+        if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
+          int noff = 0;
+          if (lane == 0) {
+            noff = gs.pool_top;
+            if (noff + 2 * tcap > P.pool_recs) gs.abort_code = IGP_E_CAPACITY;
+            else gs.pool_top = noff + 2 * tcap;
+          }
+          noff = __shfl_sync(FULL, noff, 0);
+          __syncwarp();
+          if (gs.abort_code == 0) {
+            for (int r = lane; r < nres; r += 32) {
+#pragma unroll
+              for (int f = 0; f < R_NF; ++f)
+                rec[(size_t)(noff + r) * R_NF + f] = rec[(size_t)(off + r) * R_NF + f];
+              frec[(size_t)(noff + r) * 2] = frec[(size_t)(off + r) * 2];
+              frec[(size_t)(noff + r) * 2 + 1] = frec[(size_t)(off + r) * 2 + 1];
+              meta[noff + r] = meta[off + r];
+            }
+            if (lane == 0) {
+              goff[j] = noff;
+              gcap[j] = 2 * tcap;
+            }
+            off = noff;
+          }
+          __syncwarp();
+        }
+        if (gs.abort_code == 0) {
+          const double dnext = delta_sch(hw, n + 1);
+          int part = 0;
+          for (int r = lane; r < n; r += 32) {
+            const int nu = lu[r];
+            double *rr = rec + (size_t)(off + r) * R_NF;
+            if (r < nres) {
+              Meta mt = meta[off + r];
+              if (nu != (int)mt.u) {
+                const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
+                rr[R_KA] = so.ka;
+                rr[R_CA] = so.ca;
+                rr[R_PW] = so.pw;
+                frec[(size_t)(off + r) * 2] = so.pw;
+                frec[(size_t)(off + r) * 2 + 1] = so.ca;
+                mt.u = (uint16_t)nu;
+                meta[off + r] = mt;
+              }
+              const double *ce = cold + (size_t)mt.k * C_NF;
+              rr[R_TSN] = (ce[C_KSCH] + dnext) * ce[C_NK];
+            } else {
+              const Solo so = (nu == need) ? Solo{nw_ka, nw_pw, nw_ca, 0}
+                                           : solo_lookup(tbl, cold, hw, k, need, nu);
+              rr[R_KA] = so.ka;
+              rr[R_CA] = so.ca;
+              rr[R_PW] = so.pw;
+              rr[R_TSN] = (ksch + dnext) * nkern;
+              rr[R_ACACHE] = nw_acache;
+              rr[R_TLOAD] = nw_tload;
+              rr[R_TFB] = nw_tfb;
+              rr[R_THALF] = nw_thalf;
+              frec[(size_t)(off + r) * 2] = so.pw;
+              frec[(size_t)(off + r) * 2 + 1] = so.ca;
+              meta[off + r] = Meta{k, (uint16_t)nu, (uint16_t)need};
+            }
+            part += nu;
+          }
+          part = warp_sum(part);
+          __syncwarp();
+          if (lane == 0) {
+            gstate[j] = (uint32_t)part | ((uint32_t)n << 16);
+            // prefix fold states of this GPU, in resident order
+            Neumaier fp, fc;
+            fp.s = fp.c = fc.s = fc.c = 0.0;
+            for (int r = 0; r < n; ++r) {
+              double *pp = pfx + (size_t)(off + r) * 4;
+              pp[0] = fp.s;
+              pp[1] = fp.c;
+              pp[2] = fc.s;
+              pp[3] = fc.c;
+              fp.add(frec[(size_t)(off + r) * 2]);
+              fc.add(frec[(size_t)(off + r) * 2 + 1]);
+            }
+            double *gf = gfold + (size_t)j * 4;
+            gf[0] = fp.s;
+            gf[1] = fp.c;
+            gf[2] = fc.s;
+            gf[3] = fc.c;
+          }
+        }
+      }
+    }
+    if (bk == NO_KEY) G += 1;
+    __threadfence_block();
+    group_sync<GW>();
+    if (gs.abort_code) {
+      fail_code = 2;
+      break;
+    }
+  }
+
+  // group totals of the counters
+  if (t == 0) gs.tot[0] = gs.tot[1] = gs.tot[2] = 0;
+  group_sync<GW>();
+  atomicAdd(&gs.tot[0], (unsigned long long)tot_evals);
+  atomicAdd(&gs.tot[1], (unsigned long long)tot_calls);
+  atomicAdd(&gs.tot[2], (unsigned long long)tot_cands);
+  group_sync<GW>();
+  if (t == 0 && P.stats) {
+    const bool st_ok = (P.flags & IGP_F_STATS) || fail_code == 1;
+    P.stats[4 * s] = st_ok ? (long long)gs.tot[0] : -1;
+    P.stats[4 * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
+    P.stats[4 * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
+    P.stats[4 * s + 3] = (long long)gs.tot[1];
+  }
+
+  if (fail_code) {
+    if (t == 0) {
+      if (fail_code == 1) {
+        err->code = eo_fail.code;
+        err->workload = (int)cold[(size_t)eo_fail.k * C_NF + C_WIN];
+        err->a = eo_fail.a;
+        err->b = eo_fail.b;
+        err->c = eo_fail.c;
+      } else {
+        err->code = gs.abort_code;
+        err->workload = -1;
+        err->a = (double)P.pool_recs;
+        err->b = err->c = 0.0;
+      }
+      err->gpu = -1;
+      P.gpu_count[s] = G;
+    }
+    continue;
+  }
+
+  // ---- _build_plan (planner.py:218-246): predict_gpu per device (model.py:320-343) ----
+  if (t == 0) gs.err_gpu = INT_MAX;
+  group_sync<GW>();
+  int my_err_gpu = INT_MAX;
+  ErrOut my_eo;
+  my_eo.code = 0;
+  my_eo.k = -1;
+  const bool want_pred = P.pred && !(P.flags & IGP_F_NO_PRED);
+  for (int j = t; j < G; j += GT) {
+    const int n = (int)(gstate[j] >> 16);
+    const int off = goff[j];
+    // capacity check: sum(a.r) with a.r = u * r_unit (model.py:331-335)
+    Neumaier cs;
+    cs.first((double)meta[off].u * hw.runit);
+    for (int qq = 1; qq < n; ++qq) cs.add((double)meta[off + qq].u * hw.runit);
+    const double total_r = cs.result();
+    int ecode = 0;
+    if (total_r > hw.rmax + 1e-9) {
+      ecode = IGP_E_OVERALLOC;
+      if (j < my_err_gpu) {
+        my_err_gpu = j;
+        my_eo.code = ecode;
+        my_eo.k = -1;
+        my_eo.a = total_r;
+        my_eo.b = hw.rmax;
+        my_eo.c = 0.0;
+      }
+    }
+    Neumaier fp, fc;
+    for (int qq = 0; qq < n; ++qq) {
+      const Meta mt = meta[off + qq];
+      const Solo so = solo_from_cold(cold + (size_t)mt.k * C_NF, (double)mt.u * hw.runit);
+      if (!ecode && so.err) {
+        ecode = so.err;
+        if (j < my_err_gpu) {
+          my_err_gpu = j;
+          err_operands(hw, cold + (size_t)mt.k * C_NF, mt.u, so.err, my_eo);
+          my_eo.k = mt.k;
+        }
+      }
+      L.ka[qq] = so.ka;
+      L.ca[qq] = so.ca;
+      L.pw[qq] = so.pw;
+      if (qq == 0) {
+        fp.first(so.pw);
+        fc.first(so.ca);
+      } else {
+        fp.add(so.pw);
+        fc.add(so.ca);
+      }
+    }
+    const double f = frequency(hw, hw.pidle + fp.result());
+    const double C = fc.result();
+    const double scale = f / hw.fmax;
+    const double dl = delta_sch(hw, n);
+    for (int qq = 0; qq < n; ++qq) {
+      const Meta mt = meta[off + qq];
+      const double *ce = cold + (size_t)mt.k * C_NF;
+      const double *rr = rec + (size_t)(off + qq) * R_NF;
+      const int w_in = (int)ce[C_WIN];
+      P.gpu_of[sm + w_in] = j;
+      P.pos[sm + w_in] = qq;
+      P.units[sm + w_in] = mt.u;
+      if (want_pred) {
+        const double t_sch = (ce[C_KSCH] + dl) * ce[C_NK];
+        const double t_act = L.ka[qq] * (1.0 + rr[R_ACACHE] * (C - L.ca[qq]));
+        const double t_gpu = (t_sch + t_act) / scale;
+        const double t_inf = (rr[R_TLOAD] + t_gpu) + rr[R_TFB];
+        double *row = P.pred + (sm + w_in) * 10;
+        row[0] = rr[R_TLOAD];
+        row[1] = t_sch;
+        row[2] = t_act;
+        row[3] = f;
+        row[4] = t_gpu;
+        row[5] = rr[R_TFB];
+        row[6] = t_inf;
+        row[7] = (ce[C_BATCH] / (t_gpu + rr[R_TFB])) * 1000.0;
+        row[8] = L.pw[qq];
+        row[9] = L.ca[qq];
+      }
+    }
+  }
+  if (my_err_gpu != INT_MAX) atomicMin(&gs.err_gpu, my_err_gpu);
+  group_sync<GW>();
+  const int eg = gs.err_gpu;
+  if (eg != INT_MAX && my_err_gpu == eg) {
+    err->code = my_eo.code;
+    err->workload = my_eo.k >= 0 ? (int)cold[(size_t)my_eo.k * C_NF + C_WIN] : -1;
+    err->gpu = eg;
+    err->a = my_eo.a;
+    err->b = my_eo.b;
+    err->c = my_eo.c;
+  }
+  if (t == 0) {
+    if (eg == INT_MAX) {
+      err->code = 0;
+      err->workload = -1;
+      err->gpu = -1;
+      err->a = err->b = err->c = 0.0;
+    }
+    P.gpu_count[s] = G;
+  }
+  group_sync<GW>();
+  }  // persistent scenario loop
+}
+
+}  // namespace igp

@@ -1,21 +1,44 @@
-"""Ad-hoc timing of the plan kernel on synthetic 10k scenario batches."""
-import sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-import numpy as np, torch
-from paper_2211_01713_b200 import synth, _device
-from paper_2211_01713_b200.planner import name_ranks, IGP_F_CTA
-from paper_2211_01713_b200.layout import hw_vector
-from instances import make_v100
+"""Ad-hoc timing of prepare+place (device-resident inputs, CUDA events).
 
-hw = make_v100()
-for S, m, flags in [(1, 10000, 0), (1, 10000, IGP_F_CTA), (148, 10000, 0), (592, 10000, 0), (1184, 10000, 0), (4096, 1000, 0)]:
-    wl, names = synth.scenarios(S, m, hw, seed=1)
-    rank = name_ranks(list(names))
-    _device.plan_device(wl[:1], hw_vector(hw), 32, rank, flags=flags, want_pred=False)
+usage: python tools/quick_time.py S,m,flags [S,m,flags ...]   (IGP_LIB selects a variant)"""
+import ctypes, os, sys
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import numpy as np, torch
+from paper_2211_01713_b200 import _device, _native, synth
+from paper_2211_01713_b200.layout import hw_vector
+from paper_2211_01713_b200.model import HardwareProfile
+from paper_2211_01713_b200.planner import name_ranks
+
+hw = HardwareProfile("v100", 300.0, 1530.0, 53.5, 10.0, -1.025, 0.00475, -0.00902, r_unit=0.025, price_per_hour=3.06)
+hv = np.array(hw_vector(hw))
+lib = _native.lib_for_compute()
+dev = torch.device("cuda", 0)
+P = _device._ptr
+cfgs = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]] or [(2368, 10000, 0)]
+for S, m, flags in cfgs:
+    wl, names = synth.scenarios(S, m, hw, seed=2211)
+    d_wl = torch.from_numpy(wl).to(dev)
+    d_rk = torch.from_numpy(name_ranks(list(names))).to(dev)
+    i32 = torch.empty((5, S, m), dtype=torch.int32, device=dev)
+    d_gc = torch.empty(S, dtype=torch.int32, device=dev)
+    d_st = torch.empty((S, 4), dtype=torch.int64, device=dev)
+    d_err = torch.empty((S, 40), dtype=torch.uint8, device=dev)
+    ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, 32, flags), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    def call(fn):
+        rc = fn(P(d_wl), S, m, _device._np_ptr(hv), 32, P(d_rk), 0, P(i32[0]), P(i32[1]), P(i32[2]), P(i32[3]),
+                P(i32[4]), ctypes.c_void_p(0), P(d_gc), P(d_st), P(d_err), P(ws), ws.numel(), flags,
+                ctypes.c_void_p(st.cuda_stream))
+        assert rc == 0
+    call(lib.igp_plan_batch_device); torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record(); call(lib.igp_plan_prepare_device); e[1].record(); call(lib.igp_plan_place_device); e[2].record()
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    res = _device.plan_device(wl, hw_vector(hw), 32, rank, flags=flags, want_pred=False)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t
-    print(f"S={S} m={m} flags={flags}: {dt:.3f}s  {S/dt:.2f} plans/s  gpus={res['gpu_count'][:3]} err={np.unique(res['err']['code'])}", flush=True)
+    place = e[1].elapsed_time(e[2]); prep = e[0].elapsed_time(e[1])
+    stats = d_st.cpu().numpy()
+    print(f"[{os.path.basename(_native.LIB_PATH)}] S={S} m={m} fl={flags}: place {place:.1f} ms prep {prep:.1f} ms "
+          f"-> {S/((place+prep)/1e3):.1f} plans/s; evals_run/scen={stats[:,3].mean():.0f} "
+          f"gpus={d_gc[:3].tolist()} err={np.unique(d_err.cpu().numpy().view(_native.err_dtype())['code'])}", flush=True)
+    del ws, d_wl, i32
+    torch.cuda.empty_cache()
