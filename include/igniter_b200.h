@@ -17,6 +17,9 @@
  *   igp_alloc_units_device
  *       replaces _alloc_units      planner.py:133-162 behind alloc_gpus
  *                                  planner.py:165-192
+ *   igp_solo_grid_device
+ *       replaces _Search.best_group_alloc oracle.py:77-114 for one-workload
+ *                                  groups over every batch (the solo grid)
  *   igp_prologue_device
  *       replaces appropriate_batch planner.py:76-92 and _lower_bound_units
  *                                  planner.py:95-120 (lower_bound_resources
@@ -188,6 +191,24 @@ int igp_alloc_units_device(const double *wl, int n_rows, const int32_t *batch,
 int igp_prologue_device(const double *wl, int m, const double *hw, int b_max,
                         const int32_t *batch_in, int32_t *batch, int32_t *lb, int32_t *code,
                         igp_error *err, void *stream);
+
+/*
+ * Solo candidate grid (BASELINE config 3): every (workload w, batch b in
+ * 1..b_max, units u in 1..max_units) single-entry state of _eval_entries
+ * (model.py:273-317) under the feasibility predicate of _Search._feasible
+ * (oracle.py:64-75: t_inf <= t_half and throughput >= rate_rps), with the
+ * entry built at batch b (_Entry model.py:253-270).  Replaces, per (w, b),
+ * _Search.best_group_alloc([w]) (oracle.py:77-114): the scan over u ascends
+ * and stops at the first feasible point.
+ *   wl          [16][m] fp64
+ *   min_units   [m][b_max] int32: smallest feasible u, 0 if none, or -code if
+ *               an evaluation raised first (IGP_E_DENOM / IGP_E_ACTIVE_TIME)
+ *   best_u/b    [m] int32 (nullable): cheapest feasible point, min u then min b
+ *   n_evals     device uint64 (nullable): points evaluated
+ */
+int igp_solo_grid_device(const double *wl, int m, const double *hw, int b_max,
+                         int32_t *min_units, int32_t *best_u, int32_t *best_b,
+                         unsigned long long *n_evals, void *stream);
 
 #ifdef __cplusplus
 }

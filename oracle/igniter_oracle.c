@@ -497,3 +497,36 @@ int igo_plan_batch(const double *wl, int n_scen, int m, const double *hw, int b_
   free(jobs);
   return rc;
 }
+
+/* ---- solo candidate grid: oracle.py:64-114 for one-workload groups ----
+ * For every (w, b in 1..b_max): scan u = 1..cap like _Search.best_group_alloc
+ * (oracle.py:77-114) and record the first u passing _Search._feasible
+ * (oracle.py:64-75) on the single-entry state _eval_entries([_Entry(b)], [u*r_unit]);
+ * 0 if none, -code if an evaluation raised first. */
+int igo_solo_grid(const double *wl, int64_t ld, int m, const double *hw, int b_max,
+                  int32_t *min_units, int64_t *n_evals) {
+  int cap = igo_max_units(hw);
+  int64_t ev = 0;
+  for (int w = 0; w < m; ++w) {
+    for (int b = 1; b <= b_max; ++b) {
+      entry_t e;
+      make_entry(&e, wl, ld, w, b, hw);
+      const entry_t *ep = &e;
+      double rate = WLF(wl, ld, F_RATE, w);
+      int res = 0;
+      for (int u = 1; u <= cap; ++u) {
+        double r = (double)u * hw[H_RUNIT], row[10], scratch[3];
+        igo_err err;
+        ++ev;
+        int rc = eval_entries(&ep, &r, 1, hw, row, NULL, scratch, &err);
+        if (rc) { res = -rc; break; }
+        if (row[6] > e.t_half || row[7] < rate) continue;
+        res = u;
+        break;
+      }
+      min_units[(int64_t)w * b_max + (b - 1)] = res;
+    }
+  }
+  if (n_evals) *n_evals = ev;
+  return 0;
+}

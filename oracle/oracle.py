@@ -128,3 +128,15 @@ def alloc_units(wl, batch, r, ptr, hw):
     rc = lib().igo_alloc_units(_p(wl), ctypes.c_int64(n), _p(batch), _p(r), _p(ptr),
                                ctypes.c_int(len(ptr) - 1), _p(hw), _p(units), ctypes.byref(err))
     return units, int(rc)
+
+
+def solo_grid(wl, hw, b_max: int):
+    """min feasible units per (workload, batch) -- oracle.py:64-114 semantics."""
+    wl = np.ascontiguousarray(wl, np.float64)
+    m = wl.shape[1]
+    hw = np.ascontiguousarray(hw, np.float64)
+    out = np.zeros((m, b_max), np.int32)
+    ev = np.zeros(1, np.int64)
+    lib().igo_solo_grid(_p(wl), ctypes.c_int64(m), ctypes.c_int(m), _p(hw), ctypes.c_int(b_max),
+                        _p(out), _p(ev))
+    return out, int(ev[0])

@@ -252,3 +252,27 @@ def prologue(wl, hw_vec, b_max, batch_in=None, device=None):
         on = o.cpu().numpy()[:, :m]
         err = d_err.cpu().numpy().view(_native.err_dtype())[0]
     return on[0], on[1], on[2], err
+
+
+def solo_grid(wl, hw_vec, b_max, device=None, count_evals=True):
+    """Solo candidate grid: min feasible units per (workload, batch) plus the
+    cheapest point per workload (igp_solo_grid_device)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.asarray(wl, np.float64)
+    m = wl.shape[1]
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d_wl = _to_dev(wl, device)
+        d_min = torch.empty((max(m, 1), b_max), dtype=torch.int32, device=device)
+        d_best = torch.empty((2, max(m, 1)), dtype=torch.int32, device=device)
+        d_ev = torch.zeros(1, dtype=torch.int64, device=device) if count_evals else None
+        rc = lib.igp_solo_grid_device(_ptr(d_wl), m, _np_ptr(h), int(b_max), _ptr(d_min),
+                                      _ptr(d_best[0]), _ptr(d_best[1]), _ptr(d_ev),
+                                      _stream(device))
+        _check(rc)
+        out = dict(min_units=d_min.cpu().numpy()[:m], best_u=d_best[0].cpu().numpy()[:m],
+                   best_b=d_best[1].cpu().numpy()[:m])
+        out["evals"] = int(d_ev.item()) if count_evals else -1
+    return out

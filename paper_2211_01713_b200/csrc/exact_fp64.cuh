@@ -38,9 +38,12 @@ struct Neumaier {
     c = 0.0;
   }
   __device__ __forceinline__ void add(double x) {
-    double t = s + x;
-    if (fabs(s) >= fabs(x)) c += (s - t) + x;
-    else c += (x - t) + s;
+    const double t = s + x;
+    // c += (s - t) + x if |s| >= |x| else (x - t) + s: same operations on
+    // selected operands, branch-free
+    const bool big = fabs(s) >= fabs(x);
+    const double a = big ? s : x, b = big ? x : s;
+    c += (a - t) + b;
     s = t;
   }
   __device__ __forceinline__ double result() const {

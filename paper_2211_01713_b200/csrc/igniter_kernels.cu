@@ -32,9 +32,6 @@ namespace igp {
 #define IGP_MINB_WARP 4
 #endif
 
-constexpr unsigned FULL = 0xffffffffu;
-constexpr unsigned long long NO_KEY = ~0ull;
-
 static thread_local char g_last_err[256] = "";
 
 static Hw make_hw(const double *h, int b_max) {
@@ -132,6 +129,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 }  // namespace igp
 
 #include "place.cuh"
+#include "grid.cuh"
 
 namespace igp {
 
@@ -350,6 +348,11 @@ static int cuda_fail(cudaError_t e) {
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+template <int GW>
+static size_t place_smem() {
+  return (size_t)(GW == 1 ? 128 : GW * 32) * sizeof(LaneSlot);
+}
+
 template <int MAXN, int GW>
 static unsigned place_grid(int S) {
   // persistent launch: at most as many groups as can be co-resident
@@ -358,8 +361,11 @@ static unsigned place_grid(int S) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_place<MAXN, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)place_smem<GW>());
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place<MAXN, GW>,
-                                                      GW == 1 ? 128 : GW * 32, 0) != cudaSuccess ||
+                                                      GW == 1 ? 128 : GW * 32,
+                                                      place_smem<GW>()) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
   }
@@ -373,9 +379,9 @@ template <int MAXN>
 static void launch_place(const PlanParams &P, cudaStream_t st) {
   cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
   if (P.flags & IGP_F_CTA) {
-    k_place<MAXN, 8><<<place_grid<MAXN, 8>(P.S), 256, 0, st>>>(P);
+    k_place<MAXN, 8><<<place_grid<MAXN, 8>(P.S), 256, place_smem<8>(), st>>>(P);
   } else {
-    k_place<MAXN, 1><<<place_grid<MAXN, 1>(P.S), 128, 0, st>>>(P);
+    k_place<MAXN, 1><<<place_grid<MAXN, 1>(P.S), 128, place_smem<1>(), st>>>(P);
   }
 }
 
@@ -420,8 +426,8 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.cold = (double *)(ws + L.cold);
   P.nw = (double *)(ws + L.nw);
   P.tbl = (double *)(ws + L.tbl);
-  P.gstate = (uint32_t *)(ws + L.gstate);
-  P.goff = (int32_t *)(ws + L.goff);
+  P.gstate = (unsigned long long *)(ws + L.gstate);
+  P.gstride = L.gstride;
   P.gcap = (int32_t *)(ws + L.gcap);
   P.gfold = (double *)(ws + L.gfold);
   P.rec = (double *)(ws + L.rec);
@@ -583,6 +589,30 @@ int igp_prologue_device(const double *wl, int m, const double *hw_h, int b_max,
   if (m > 0) k_prologue<<<nblk(m, 256), 256, 0, st>>>(wl, m, hw, batch_in, batch, lb, code, fe);
   k_prologue_err<<<1, 1, 0, st>>>(wl, m, hw, batch_in, fe, err);
   CK(cudaFreeAsync(fe, st));
+  CK(cudaGetLastError());
+  return IGP_E_OK;
+}
+
+int igp_solo_grid_device(const double *wl, int m, const double *hw_h, int b_max,
+                         int32_t *min_units, int32_t *best_u, int32_t *best_b,
+                         unsigned long long *n_evals, void *stream) {
+  if (m < 0 || b_max < 1 || !hw_h) return IGP_E_ARG;
+  Hw hw = make_hw(hw_h, b_max);
+  if (hw.cap < 1) return IGP_E_ARG;
+  if (m == 0) return IGP_E_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  GridParams G;
+  G.hw = hw;
+  G.m = m;
+  G.b_max = b_max;
+  G.wl = wl;
+  G.min_units = min_units;
+  G.best_u = best_u;
+  G.best_b = best_b;
+  G.evals = n_evals;
+  if (n_evals) CK(cudaMemsetAsync(n_evals, 0, sizeof(unsigned long long), st));
+  k_solo_grid<<<nblk((long long)m * b_max, 256), 256, 0, st>>>(G);
+  if (best_u && best_b) k_grid_best<<<nblk((long long)m * 32, 256), 256, 0, st>>>(G);
   CK(cudaGetLastError());
   return IGP_E_OK;
 }

@@ -31,7 +31,11 @@ namespace igp {
 
 constexpr int TB = 16;     // solo-table entries per workload
 constexpr int TILE0 = 4;   // initial tile capacity
-enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_NF };
+// pool record of one resident (96 B): its solo terms at the committed units,
+// t_sch for the next candidate size, the transfer / budget constants, and the
+// solo terms one unit up (a first bump inside a candidate needs no lookup)
+enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_KA1, R_PW1, R_CA1,
+       R_ERR1, R_NF };
 enum { SF_RISKY = 1, SF_NO_MARGIN = 2 };
 enum { R_FEAS = 0, R_INFEAS = 1, R_PRUNED = 2, R_ERROR = 3 };
 
@@ -41,10 +45,78 @@ struct Meta {
   uint16_t lb;
 };
 
+// A candidate's resident tile is staged into a per-lane shared-memory slot
+// with one TMA bulk copy (records, meta, the GPU's Neumaier fold state);
+// residents beyond SLOT are read from the global pool.
+#ifndef IGP_SLOT
+#define IGP_SLOT 3
+#endif
+constexpr int SLOT = IGP_SLOT;
+constexpr int SLOT_META = (SLOT + 1) & ~1;
+constexpr int QN = 128;  // per-warp candidate ring queue
+
+struct __align__(16) LaneSlot {
+  double rec[SLOT][R_NF];
+  Meta meta[SLOT_META];
+  double gf[4];
+  unsigned long long mbar;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// non-blocking completion test of the phase with the given parity
+__device__ __forceinline__ bool mbar_test(unsigned long long *bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// bulk prefetch into L2 (no shared memory, no completion to wait for)
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// generic-proxy writes -> later async-proxy (TMA) access of the same memory
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 struct WsLayout {
-  size_t by_rank, order, cold, nw, tbl, gstate, goff, gcap, gfold, rec, frec, pfx, meta,
+  size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
       lane_units, sflags, perr, sched, total;
   int lanes;
+  int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
 };
 
@@ -69,8 +141,8 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.cold = off; off = align_up(off + Sm * C_NF * 8);
   L.nw = off; off = align_up(off + Sm * R_NF * 8);
   L.tbl = off; off = align_up(off + Sm * TB * 4 * 8);
-  L.gstate = off; off = align_up(off + Sm * 4);
-  L.goff = off; off = align_up(off + Sm * 4);
+  L.gstride = (int)((mm + 3) & ~(size_t)3);
+  L.gstate = off; off = align_up(off + (size_t)S * L.gstride * 8);
   L.gcap = off; off = align_up(off + Sm * 4);
   L.gfold = off; off = align_up(off + Sm * 4 * 8);
   L.rec = off; off = align_up(off + Sp * R_NF * 8);
@@ -92,11 +164,13 @@ struct PlanParams {
   const int32_t *rank;  // name ranks
   int rank_stride;
   int lanes;
+  int gstride;
   long long pool_recs;
   // workspace
-  int32_t *by_rank, *order, *sflags, *perr, *goff, *gcap;
+  int32_t *by_rank, *order, *sflags, *perr, *gcap;
   int32_t *sched;  // persistent-kernel scenario counter (zeroed before each launch)
-  uint32_t *gstate;
+  // per open GPU j: occupied units | residents << 16 | tile offset << 32
+  unsigned long long *gstate;
   double *cold, *nw, *tbl, *gfold, *rec, *frec, *pfx;
   Meta *meta;
   uint16_t *lane_units;
@@ -270,7 +344,7 @@ __device__ __forceinline__ int warp_sum(int v) {
 __device__ __forceinline__ Solo solo_lookup(const double *tbl, const double *cold, const Hw &hw,
                                             int k, int lb, int u) {
   const int v = u - lb;
-  if (v >= 0 && v < TB) {
+  if (v >= 0 && v < TB && u <= hw.cap) {
     const double *t = tbl + ((size_t)k * TB + v) * 4;
     Solo so;
     so.ka = t[0];
@@ -342,9 +416,17 @@ k_place(PlanParams P) {
   constexpr unsigned long long NO_KEY = ~0ull;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ GroupSmem gsm[GPB];
-  __shared__ int qsm[GPB * GW][64];
+  __shared__ int qsm[GPB * GW][QN];
+  __shared__ unsigned long long qgs[GPB * GW][QN];
+  __shared__ double ntb[GPB][TB * 4];  // the newcomer's solo table row
+  extern __shared__ __align__(16) unsigned char dsm[];
   const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
   GroupSmem &gs = gsm[grp];
+  LaneSlot *const sl = reinterpret_cast<LaneSlot *>(dsm) + threadIdx.x;
+  mbar_init(&sl->mbar);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  uint32_t c_phase = 0;  // parity of this lane's mbarrier
   // Persistent groups: each pulls the next scenario when it finishes one, so
   // scenarios of unequal length do not leave SMs idle at the end.
   for (;;) {
@@ -354,6 +436,8 @@ k_place(PlanParams P) {
   group_sync<GW>();
   if (s >= P.S) break;
   int *q = qsm[grp * GW + wi];
+  unsigned long long *qg = qgs[grp * GW + wi];
+  double *ntab = ntb[grp];
   const Hw &hw = P.hw;
   const int m = P.m, cap = hw.cap;
   const size_t sm = (size_t)s * m;
@@ -387,8 +471,7 @@ k_place(PlanParams P) {
   const double *cold = P.cold + sm * C_NF;
   const double *nwt = P.nw + sm * R_NF;
   const double *tbl = P.tbl + sm * TB * 4;
-  uint32_t *gstate = P.gstate + sm;
-  int32_t *goff = P.goff + sm;
+  unsigned long long *gstate = P.gstate + (size_t)s * P.gstride;
   int32_t *gcap = P.gcap + sm;
   double *gfold = P.gfold + sm * 4;
   const size_t sp = (size_t)s * (size_t)P.pool_recs;
@@ -430,6 +513,12 @@ k_place(PlanParams P) {
       gs.best = NO_KEY;
       gs.err_flag = 0;
     }
+    for (int x = t; x < TB * 4; x += GT) ntab[x] = tbl[(size_t)k * TB * 4 + x];
+    if (t == 0 && k + 1 < m) {  // the next newcomer's rows
+      prefetch_l2(cold + (size_t)(k + 1) * C_NF, C_NF * 8);
+      prefetch_l2(nwt + (size_t)(k + 1) * R_NF, R_NF * 8);
+      prefetch_l2(tbl + (size_t)(k + 1) * TB * 4, TB * 32);
+    }
     group_sync<GW>();
     unsigned long long my_best = NO_KEY;
 
@@ -444,15 +533,24 @@ k_place(PlanParams P) {
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
     auto run_step = [&](const bool serial) {
       int qhead = 0, qtail = 0;
-      int scan = serial ? 0 : wi * 32;
-      const int scan_stride = serial ? 32 : GT;
+      int scan = serial ? 0 : wi * 64;
+      const int scan_stride = serial ? 64 : GT * 2;
       const unsigned take_mask = serial ? 1u : FULL;
       int cj = -1, c_nres = 0, c_occ = 0, c_sum = 0, c_i = 0, c_dirty = 0, c_off = 0;
       int c_pend = -1, c_pcode = 0, c_nu = 0;
-      bool c_flag = false, c_need = false;
+      unsigned c_sb = 0;  // staged residents already bumped inside this candidate
+      bool c_flag = false, c_need = false, c_wait = false;
       double c_C = 0.0, c_scale = 1.0, c_inv = 1.0, c_tsn = 0.0;
       double c_nka = 0.0, c_npw = 0.0, c_nca = 0.0;
       bool stop = false;
+
+      auto prefetch_tile = [&](unsigned long long g, int j) {
+        const int nr = (int)((g >> 16) & 0xffffu), of = (int)(g >> 32);
+        const int nst = nr < SLOT ? nr : SLOT;
+        prefetch_l2(rec + (size_t)of * R_NF, (uint32_t)nst * (R_NF * 8));
+        prefetch_l2(meta + of, (uint32_t)((nst + 1) >> 1) * 16u);
+        prefetch_l2(gfold + (size_t)j * 4, 32u);
+      };
 
       auto finish = [&](int result) {
         if (result == R_ERROR) {
@@ -462,6 +560,10 @@ k_place(PlanParams P) {
             if (c_pend == c_nres) {
               ek = k;
               eu = c_nu;
+            } else if (c_pend < SLOT) {
+              const Meta mt = sl->meta[c_pend];
+              ek = mt.k;
+              eu = (int)mt.u;
             } else {
               const Meta mt = meta[c_off + c_pend];
               ek = mt.k;
@@ -478,7 +580,8 @@ k_place(PlanParams P) {
             my_best = key;
             uint16_t *lu = lane_units + (size_t)t * cap;
             for (int qq = 0; qq < c_nres; ++qq)
-              lu[qq] = mod.test(qq) ? (uint16_t)L.u[qq] : meta[c_off + qq].u;
+              lu[qq] = qq < SLOT ? sl->meta[qq].u
+                                 : (mod.test(qq) ? (uint16_t)L.u[qq] : meta[c_off + qq].u);
             lu[c_nres] = (uint16_t)c_nu;
           }
           atomicMin(&gs.best, key);
@@ -492,28 +595,68 @@ k_place(PlanParams P) {
         const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
         if (idle) {
           const int nidle = __popc(idle);
+          // prefilter occupied + need <= cap (planner.py:297-299): two GPU
+          // descriptors per lane per 16-byte load; passing (j, descriptor)
+          // pairs are appended in ascending j
           while (qtail - qhead < nidle && scan < G) {
-            const int jj = scan + lane;
-            const bool pass = (jj < G) && ((int)(gstate[jj] & 0xffffu) + need <= cap);
-            const unsigned mask = __ballot_sync(FULL, pass);
-            if (pass) q[(qtail + __popc(mask & lt)) & 63] = jj;
-            qtail += __popc(mask);
+            const int jb = scan + lane * 2;
+            unsigned bits = 0;
+            ulonglong2 g2 = make_ulonglong2(0ull, 0ull);
+            if (jb < G) {
+              g2 = *reinterpret_cast<const ulonglong2 *>(gstate + jb);
+              const int lim = cap - need;
+              bits = ((int)(g2.x & 0xffffu) <= lim ? 1u : 0u) |
+                     ((jb + 1 < G && (int)(g2.y & 0xffffu) <= lim) ? 2u : 0u);
+            }
+            const int cnt = __popc(bits);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(FULL, incl, o);
+              if (lane >= o) incl += v;
+            }
+            int qp = qtail + incl - cnt;
+            // queued candidates are taken some iterations later: start pulling
+            // their tiles into L2 now so the lane's tile copy is an L2 hit
+            if (bits & 1u) {
+              q[qp & (QN - 1)] = jb;
+              qg[qp & (QN - 1)] = g2.x;
+              ++qp;
+              prefetch_tile(g2.x, jb);
+            }
+            if (bits & 2u) {
+              q[qp & (QN - 1)] = jb + 1;
+              qg[qp & (QN - 1)] = g2.y;
+              prefetch_tile(g2.y, jb + 1);
+            }
+            qtail += __shfl_sync(FULL, incl, 31);
             scan += scan_stride;
           }
           __syncwarp();
           if ((idle >> lane) & 1u) {
             const int r = __popc(idle & lt);
             if (qhead + r < qtail) {
-              const int j = q[(qhead + r) & 63];
+              const int j = q[(qhead + r) & (QN - 1)];
+              const unsigned long long g = qg[(qhead + r) & (QN - 1)];
               st_cands += 1;
               const volatile unsigned long long *bp = &gs.best;
               if (exact || ((((unsigned long long)need) << 32) | (unsigned)j) <= *bp) {
                 // residents_j + [newcomer] (planner.py:302-304)
-                const uint32_t g = gstate[j];
                 cj = j;
                 c_occ = (int)(g & 0xffffu);
-                c_nres = (int)(g >> 16);
-                c_off = goff[j];
+                c_nres = (int)((g >> 16) & 0xffffu);
+                c_off = (int)(g >> 32);
+                {  // stage the resident tile: one bulk copy group per candidate
+                  const int nst = c_nres < SLOT ? c_nres : SLOT;
+                  const uint32_t brec = (uint32_t)nst * (R_NF * 8);
+                  const uint32_t bmeta = (uint32_t)((nst + 1) >> 1) * 16u;
+                  fence_async_smem();
+                  mbar_expect_tx(&sl->mbar, brec + bmeta + 32u);
+                  bulk_g2s(sl->rec, rec + (size_t)c_off * R_NF, brec, &sl->mbar);
+                  bulk_g2s(sl->meta, meta + c_off, bmeta, &sl->mbar);
+                  bulk_g2s(sl->gf, gfold + (size_t)j * 4, 32u, &sl->mbar);
+                  c_wait = true;
+                }
                 c_sum = c_occ + need;
                 c_i = 0;
                 c_dirty = c_nres;
@@ -525,6 +668,7 @@ k_place(PlanParams P) {
                 c_nca = nw_ca;
                 c_tsn = (ksch + delta_sch(hw, c_nres + 1)) * nkern;
                 mod.clear();
+                c_sb = 0;
                 c_pend = -1;
                 if (exact) {
                   for (int qq = 0; qq < c_nres && c_pend < 0; ++qq) {
@@ -553,22 +697,47 @@ k_place(PlanParams P) {
         }
         if (cj < 0) continue;
         if (c_need) {
+          if (c_wait) {
+            // the tile is not here yet: this lane sits the iteration out and
+            // the warp's other lanes go on (a blocking wait would stall them)
+            if (!mbar_test(&sl->mbar, c_phase)) continue;
+            c_phase ^= 1u;
+            c_wait = false;
+          }
           if (c_pend >= 0) {
             finish(R_ERROR);
             continue;
           }
           // _eval_entries device terms (model.py:299-305), folded in resident
-          // order from the last valid cached prefix state
-          const double *stp = (c_dirty == c_nres) ? gfold + (size_t)cj * 4
-                                                  : pfx + (size_t)(c_off + c_dirty) * 4;
+          // order: from the GPU's cached fold when nothing changed, else from
+          // the start over the staged tile (recomputing an unchanged prefix
+          // gives the cached prefix state bit for bit), else from the cached
+          // prefix state of the first changed resident beyond the slot
           Neumaier fp, fc;
-          fp.s = stp[0];
-          fp.c = stp[1];
-          fc.s = stp[2];
-          fc.c = stp[3];
-          for (int qq = c_dirty; qq < c_nres; ++qq) {
+          int q0;
+          if (c_dirty == c_nres) {
+            fp.s = sl->gf[0];
+            fp.c = sl->gf[1];
+            fc.s = sl->gf[2];
+            fc.c = sl->gf[3];
+            q0 = c_nres;
+          } else if (c_dirty < SLOT) {
+            fp.s = fp.c = fc.s = fc.c = 0.0;
+            q0 = 0;
+          } else {
+            const double *stp = pfx + (size_t)(c_off + c_dirty) * 4;
+            fp.s = stp[0];
+            fp.c = stp[1];
+            fc.s = stp[2];
+            fc.c = stp[3];
+            q0 = c_dirty;
+          }
+          for (int qq = q0; qq < c_nres; ++qq) {
             double pw, ca;
-            if (mod.test(qq)) {
+            if (qq < SLOT) {
+              pw = sl->rec[qq][R_PW];
+              ca = sl->rec[qq][R_CA];
+            } else if (mod.test(qq)) {
               pw = L.pw[qq];
               ca = L.ca[qq];
             } else {
@@ -589,9 +758,12 @@ k_place(PlanParams P) {
           st_calls += 1;
           c_need = false;
         }
-        // check resident c_i: t_inf > t_half (model.py:308-313, planner.py:158)
-        {
-          const int i = c_i;
+        // The checks this evaluation serves (model.py:308-313, planner.py:158):
+        // residents c_i, c_i+1, ... see the same device terms until one of
+        // them is bumped, so one iteration runs them all and stops at the
+        // first violation.
+        int viol = -1;
+        for (int i = c_i; i <= c_nres; ++i) {
           double ka, ca, t_sch, acache, t_load, t_fb, t_half;
           if (i == c_nres) {
             ka = c_nka;
@@ -601,6 +773,15 @@ k_place(PlanParams P) {
             t_load = nw_tload;
             t_fb = nw_tfb;
             t_half = nw_thalf;
+          } else if (i < SLOT) {
+            const double *r = sl->rec[i];
+            ka = r[R_KA];
+            ca = r[R_CA];
+            t_sch = r[R_TSN];
+            acache = r[R_ACACHE];
+            t_load = r[R_TLOAD];
+            t_fb = r[R_TFB];
+            t_half = r[R_THALF];
           } else {
             const double *r = rec + (size_t)(c_off + i) * R_NF;
             const double2 kc = *reinterpret_cast<const double2 *>(r + R_KA);
@@ -632,49 +813,82 @@ k_place(PlanParams P) {
           }
           const double t_inf = (t_load + t_gpu) + t_fb;
           if (t_inf > t_half) {
-            c_sum += 1;
-            if (!exact) {
-              // units only grow: an overflow or a key that already loses ends
-              // the candidate before any further work
-              if (c_sum > cap) {
-                finish(R_INFEAS);
-                continue;
-              }
-              const volatile unsigned long long *bp = &gs.best;
-              const unsigned long long key =
-                  ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
-              if (key > *bp) {
-                finish(R_PRUNED);
-                continue;
-              }
-            }
-            Solo so;
-            if (i == c_nres) {
-              c_nu += 1;
-              so = solo_lookup(tbl, cold, hw, k, need, c_nu);
-              c_nka = so.ka;
-              c_npw = so.pw;
-              c_nca = so.ca;
-            } else {
-              const Meta mt = meta[c_off + i];
-              const int u = (mod.test(i) ? L.u[i] : (int)mt.u) + 1;
-              so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
-              L.u[i] = u;
-              L.ka[i] = so.ka;
-              L.pw[i] = so.pw;
-              L.ca[i] = so.ca;
-              mod.set(i);
-            }
-            if (i < c_dirty) c_dirty = i;
-            if (exact && so.err && c_pend < 0) {
-              c_pend = i;
-              c_pcode = so.err;
-            }
-            c_flag = true;
-            c_need = true;
+            viol = i;
+            break;
           }
         }
-        c_i += 1;
+        if (viol < 0) {
+          c_i = c_nres + 1;  // the rest of the pass is clean
+        } else {
+          const int i = viol;
+          c_sum += 1;
+          if (!exact) {
+            // units only grow: an overflow or a key that already loses ends
+            // the candidate before any further work
+            if (c_sum > cap) {
+              finish(R_INFEAS);
+              continue;
+            }
+            const volatile unsigned long long *bp = &gs.best;
+            const unsigned long long key =
+                ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
+            if (key > *bp) {
+              finish(R_PRUNED);
+              continue;
+            }
+          }
+          Solo so;
+          if (i == c_nres) {
+            c_nu += 1;
+            const int v = c_nu - need;
+            if (v < TB && c_nu <= cap) {
+              const double *tv = ntab + v * 4;
+              so.ka = tv[0];
+              so.pw = tv[1];
+              so.ca = tv[2];
+              so.err = (int)tv[3];
+            } else {
+              so = solo_from_cold(ck, (double)c_nu * hw.runit);
+            }
+            c_nka = so.ka;
+            c_npw = so.pw;
+            c_nca = so.ca;
+          } else if (i < SLOT) {
+            const Meta mt = sl->meta[i];
+            const int u = (int)mt.u + 1;
+            if (!((c_sb >> i) & 1u)) {  // one unit above the committed units
+              const double *r = sl->rec[i];
+              so.ka = r[R_KA1];
+              so.pw = r[R_PW1];
+              so.ca = r[R_CA1];
+              so.err = (int)r[R_ERR1];
+              c_sb |= 1u << i;
+            } else {
+              so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
+            }
+            sl->meta[i].u = (uint16_t)u;
+            sl->rec[i][R_KA] = so.ka;
+            sl->rec[i][R_CA] = so.ca;
+            sl->rec[i][R_PW] = so.pw;
+          } else {
+            const Meta mt = meta[c_off + i];
+            const int u = (mod.test(i) ? L.u[i] : (int)mt.u) + 1;
+            so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
+            L.u[i] = u;
+            L.ka[i] = so.ka;
+            L.pw[i] = so.pw;
+            L.ca[i] = so.ca;
+            mod.set(i);
+          }
+          if (i < c_dirty) c_dirty = i;
+          if (exact && so.err && c_pend < 0) {
+            c_pend = i;
+            c_pcode = so.err;
+          }
+          c_flag = true;
+          c_need = true;
+          c_i = i + 1;
+        }
         if (c_i > c_nres) {
           if (c_flag && c_sum <= cap) {
             c_i = 0;
@@ -725,9 +939,8 @@ k_place(PlanParams P) {
             gs.abort_code = IGP_E_CAPACITY;
           } else {
             gs.pool_top = off + TILE0;
-            goff[G] = off;
             gcap[G] = TILE0;
-            gstate[G] = (uint32_t)need | (1u << 16);
+            gstate[G] = ((unsigned long long)off << 32) | (unsigned)need | (1u << 16);
             double *r = rec + (size_t)off * R_NF;
             r[R_KA] = nw_ka;
             r[R_CA] = nw_ca;
@@ -737,6 +950,13 @@ k_place(PlanParams P) {
             r[R_TFB] = nw_tfb;
             r[R_THALF] = nw_thalf;
             r[R_PW] = nw_pw;
+            {
+              const Solo s1 = solo_lookup(tbl, cold, hw, k, need, need + 1);
+              r[R_KA1] = s1.ka;
+              r[R_PW1] = s1.pw;
+              r[R_CA1] = s1.ca;
+              r[R_ERR1] = (double)s1.err;
+            }
             frec[(size_t)off * 2] = nw_pw;
             frec[(size_t)off * 2 + 1] = nw_ca;
             double *pp = pfx + (size_t)off * 4;
@@ -755,9 +975,9 @@ k_place(PlanParams P) {
       } else {
         const int j = (int)(bk & 0xffffffffu);
         const uint16_t *lu = lane_units + (size_t)gs.win_thread * cap;
-        const int nres = (int)(gstate[j] >> 16);
+        const int nres = (int)((gstate[j] >> 16) & 0xffffu);
         const int n = nres + 1;
-        int off = goff[j];
+        int off = (int)(gstate[j] >> 32);
         const int tcap = gcap[j];
         if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
           int noff = 0;
@@ -777,10 +997,7 @@ k_place(PlanParams P) {
               frec[(size_t)(noff + r) * 2 + 1] = frec[(size_t)(off + r) * 2 + 1];
               meta[noff + r] = meta[off + r];
             }
-            if (lane == 0) {
-              goff[j] = noff;
-              gcap[j] = 2 * tcap;
-            }
+            if (lane == 0) gcap[j] = 2 * tcap;
             off = noff;
           }
           __syncwarp();
@@ -795,9 +1012,14 @@ k_place(PlanParams P) {
               Meta mt = meta[off + r];
               if (nu != (int)mt.u) {
                 const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
+                const Solo s1 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu + 1);
                 rr[R_KA] = so.ka;
                 rr[R_CA] = so.ca;
                 rr[R_PW] = so.pw;
+                rr[R_KA1] = s1.ka;
+                rr[R_PW1] = s1.pw;
+                rr[R_CA1] = s1.ca;
+                rr[R_ERR1] = (double)s1.err;
                 frec[(size_t)(off + r) * 2] = so.pw;
                 frec[(size_t)(off + r) * 2 + 1] = so.ca;
                 mt.u = (uint16_t)nu;
@@ -808,9 +1030,14 @@ k_place(PlanParams P) {
             } else {
               const Solo so = (nu == need) ? Solo{nw_ka, nw_pw, nw_ca, 0}
                                            : solo_lookup(tbl, cold, hw, k, need, nu);
+              const Solo s1 = solo_lookup(tbl, cold, hw, k, need, nu + 1);
               rr[R_KA] = so.ka;
               rr[R_CA] = so.ca;
               rr[R_PW] = so.pw;
+              rr[R_KA1] = s1.ka;
+              rr[R_PW1] = s1.pw;
+              rr[R_CA1] = s1.ca;
+              rr[R_ERR1] = (double)s1.err;
               rr[R_TSN] = (ksch + dnext) * nkern;
               rr[R_ACACHE] = nw_acache;
               rr[R_TLOAD] = nw_tload;
@@ -825,7 +1052,7 @@ k_place(PlanParams P) {
           part = warp_sum(part);
           __syncwarp();
           if (lane == 0) {
-            gstate[j] = (uint32_t)part | ((uint32_t)n << 16);
+            gstate[j] = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
             // prefix fold states of this GPU, in resident order
             Neumaier fp, fc;
             fp.s = fp.c = fc.s = fc.c = 0.0;
@@ -848,6 +1075,7 @@ k_place(PlanParams P) {
       }
     }
     if (bk == NO_KEY) G += 1;
+    if (wi == 0) fence_async_global();  // commit writes -> next step's tile copies
     __threadfence_block();
     group_sync<GW>();
     if (gs.abort_code) {
@@ -900,8 +1128,8 @@ k_place(PlanParams P) {
   my_eo.k = -1;
   const bool want_pred = P.pred && !(P.flags & IGP_F_NO_PRED);
   for (int j = t; j < G; j += GT) {
-    const int n = (int)(gstate[j] >> 16);
-    const int off = goff[j];
+    const int n = (int)((gstate[j] >> 16) & 0xffffu);
+    const int off = (int)(gstate[j] >> 32);
     // capacity check: sum(a.r) with a.r = u * r_unit (model.py:331-335)
     Neumaier cs;
     cs.first((double)meta[off].u * hw.runit);

@@ -283,8 +283,34 @@ def denom_error_workload(name, k4, k3=-1.0, slo=40.0):
     return spec, coef
 
 
+def grid_case(workloads, hw, b_max):
+    """Per (w, b): the reference's own one-workload grid search,
+    _Search.best_group_alloc([w]) (oracle.py:77-114), with the entry built at
+    batch b.  Records the minimal feasible units, 0 if none, -code if an
+    evaluation raised (NonPositiveDenominatorError)."""
+    from gpuplanner import oracle as goracle
+    out = pack_instance(workloads, hw, b_max)
+    m = len(workloads)
+    specs = {s.name: s for s, _ in workloads}
+    budget = goracle.OracleBudget(max_candidates=10**12)
+    res = np.zeros((m, b_max), np.int32)
+    for i, (s, c) in enumerate(workloads):
+        for b in range(1, b_max + 1):
+            search = goracle._Search(specs, {s.name: gmodel._Entry(s, c, b, hw)}, hw, budget)
+            try:
+                r = search.best_group_alloc([s.name])
+            except gerr.NonPositiveDenominatorError as exc:
+                res[i, b - 1] = -err_code(exc)
+                continue
+            res[i, b - 1] = 0 if r is None else r[0]
+    out.update(min_units=res)
+    return out
+
+
 def main():
-    manifest = {}
+    groups = set(sys.argv[1:]) or {"plan", "component", "grid"}
+    mpath = os.path.join(HERE, "manifest.json")
+    manifest = json.load(open(mpath))["cases"] if os.path.exists(mpath) else {}
     v100 = support.make_v100()
 
     def save(name, d, note):
@@ -363,14 +389,38 @@ def main():
     plan_cases.append(("plan_err_denom_alone", [denom_error_workload("solo_neg", -0.5)], v100, 32,
                        "denominator error surfaced only by _build_plan/predict_gpu"))
 
-    for name, wls, hw, bmax, note in plan_cases:
+    for name, wls, hw, bmax, note in plan_cases if "plan" in groups else []:
         d, dt = run_plan_case(wls, hw, bmax)
         extra = f" [{str(d['err_class'])}]" if str(d["err_class"]) else (
             f" -> {int(d['gpu_count'])} GPUs, evals={int(d['model_evals'])}, "
             f"cands={int(d['candidate_gpus'])}, {dt:.2f}s")
         save(name, d, note + extra)
 
+    # ---- solo candidate grid (BASELINE config 3) --------------------------
+    if "grid" in groups:
+        rng = np.random.default_rng(2212)
+        c3 = [c3_feasible_workload(rng, f"g{i:03d}", hw01) for i in range(40)]
+        save("grid_c3_40", grid_case(c3, hw01, 128),
+             "solo grid: 40 C3-generator workloads x b 1..128 x u 1..100 (oracle.py:77-114)")
+        inst = support.random_instance(np.random.default_rng(2213), 60, v100)
+        save("grid_v100_60", grid_case(inst, v100, 32),
+             "solo grid: 60 random_instance workloads x b 1..32 x u 1..40")
+        odd = [denom_error_workload("gneg", -0.5), denom_error_workload("gnegk", 0.05, k3=-3.0),
+               (support.demo_spec("gfloor"), support.demo_coef(alpha_power_w=400.0, beta_power_w=300.0)),
+               (gp.WorkloadSpec("gtight", 1.0, 5000.0, 0.9, 0.05), support.demo_coef()),
+               (gp.WorkloadSpec("gloose", 200.0, 10.0, 0.0, 0.0), support.demo_coef())]
+        rngw = np.random.default_rng(2214)
+        odd += [(wide_spec(rngw, f"gw{i}"), wide_coef(rngw)) for i in range(25)]
+        save("grid_edge_30", grid_case(odd, v100, 48),
+             "solo grid edge cases: denominator / active-time errors, f_min floor, "
+             "infeasible everywhere, wide coefficients")
+
     # ---- component cases ------------------------------------------------
+    if "component" not in groups:
+        with open(mpath, "w") as fh:
+            json.dump({"python": sys.version.split()[0], "numpy": np.__version__,
+                       "cases": manifest}, fh, indent=1, sort_keys=True)
+        return
     save("eval_states_v100", eval_states_case(np.random.default_rng(101), 1000, v100),
          "1000 random device states, n=1..12, wide coefficients (_eval_entries rows)")
     save("eval_states_floor", eval_states_case(np.random.default_rng(102), 600, v100, floor_bias=True),
@@ -384,7 +434,7 @@ def main():
     save("alloc_v100", alloc_case(np.random.default_rng(106), 400, v100),
          "400 alloc_gpus calls (Alg. 2) on random residents")
 
-    with open(os.path.join(HERE, "manifest.json"), "w") as fh:
+    with open(mpath, "w") as fh:
         json.dump({"python": sys.version.split()[0], "numpy": np.__version__,
                    "cases": manifest}, fh, indent=1, sort_keys=True)
 

@@ -81,3 +81,12 @@ def test_predict_known_values_in_eval_fixture_semantics(oracle_lib):
     assert rows[0, 6] == pytest.approx(13.715733333333333, rel=1e-12)
     assert rows[0, 3] == 1530.0
     assert rows[0, 7] == pytest.approx(603.4760218860637, rel=1e-12)
+
+
+@pytest.mark.parametrize("case", G.names("grid_"))
+def test_oracle_solo_grid_matches_reference(oracle_lib, case):
+    """Solo grid vs the reference's _Search.best_group_alloc (oracle.py:77-114)."""
+    d = G.load(case)
+    mu, evals = oracle_lib.solo_grid(d["wl"], d["hw"], int(d["b_max"]))
+    np.testing.assert_array_equal(mu, d["min_units"])
+    assert evals > 0
