@@ -17,6 +17,10 @@
  *   igp_alloc_units_device
  *       replaces _alloc_units      planner.py:133-162 behind alloc_gpus
  *                                  planner.py:165-192
+ *   igp_stream_*_device
+ *       the planner.py:290-319 step applied in arrival order to persistent
+ *                                  device state (online re-provisioning; no
+ *                                  reference API, see below)
  *   igp_solo_grid_device
  *       replaces _Search.best_group_alloc oracle.py:77-114 for one-workload
  *                                  groups over every batch (the solo grid)
@@ -191,6 +195,36 @@ int igp_alloc_units_device(const double *wl, int n_rows, const int32_t *batch,
 int igp_prologue_device(const double *wl, int m, const double *hw, int b_max,
                         const int32_t *batch_in, int32_t *batch, int32_t *lb, int32_t *code,
                         igp_error *err, void *stream);
+
+/*
+ * Online re-provisioning stream (BASELINE config 5).  The reference has no
+ * API for it (plan() always sorts, planner.py:284); each arrival is one step
+ * of planner.py:290-319 in ARRIVAL order against persistent device state,
+ * with its batch and lower bound from planner.py:76-120.  An arrival whose
+ * prologue or candidate evaluation raises is rejected (code = IGP_E_*) and
+ * leaves the state unchanged.  n_streams independent streams advance
+ * together; each push appends n arrivals to every stream.  All state lives in
+ * the caller's device workspace (igp_stream_workspace_bytes); the caller
+ * tracks k0 = arrivals pushed so far.
+ *   push:      wl_new [S][16][n]; outputs [S][n]: GPU index and position
+ *              within that GPU at admission (-1 when rejected), and the code
+ *   snapshot:  [S][n_arrivals] current GPU, position and units of every
+ *              arrival (units 0 when rejected), breakdown rows (nullable),
+ *              GPU count and the predict_gpu error record per stream
+ */
+size_t igp_stream_workspace_bytes(int n_streams, int capacity, const double *hw, int b_max,
+                                  int flags);
+int igp_stream_reset_device(int n_streams, int capacity, const double *hw, int b_max,
+                            void *workspace, size_t workspace_bytes, int flags, void *stream);
+int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, int capacity,
+                           const double *hw, int b_max, int32_t *gpu_of, int32_t *pos,
+                           int32_t *code, int64_t *stats, void *workspace,
+                           size_t workspace_bytes, int flags, void *stream);
+int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, const double *hw,
+                               int b_max, int32_t *gpu_of, int32_t *pos, int32_t *units,
+                               double *pred, int32_t *gpu_count, igp_error *err,
+                               void *workspace, size_t workspace_bytes, int flags,
+                               void *stream);
 
 /*
  * Solo candidate grid (BASELINE config 3): every (workload w, batch b in

@@ -530,3 +530,98 @@ int igo_solo_grid(const double *wl, int64_t ld, int m, const double *hw, int b_m
   if (n_evals) *n_evals = ev;
   return 0;
 }
+
+/* ---- online stream: planner.py:290-319 in arrival order --------------
+ * No reference API exists (plan() always sorts, planner.py:284); this is the
+ * driver over the reference internals that tests/golden/make_golden.py
+ * (stream_reference) runs: each arrival gets its batch and lower bound
+ * (planner.py:280-282) and is placed by one Alg. 1 step against the
+ * persistent state; an arrival whose prologue or candidate evaluation
+ * raises is rejected (code = error) and leaves the state unchanged. */
+int igo_stream(const double *wl, int64_t ld, int n, const double *hw, int b_max,
+               int32_t *gpu_of, int32_t *pos, int32_t *code, int32_t *units_final,
+               int32_t *gpu_count, int64_t *stats) {
+  int cap = igo_max_units(hw);
+  int stride = cap + 1;
+  int nn = n > 0 ? n : 1;
+  entry_t *ents = malloc(sizeof(entry_t) * nn);
+  int *lbv = malloc(sizeof(int) * nn);
+  int *g_res = malloc(sizeof(int) * (size_t)nn * stride);
+  int *g_units = malloc(sizeof(int) * (size_t)nn * stride);
+  int *g_n = calloc(nn, sizeof(int));
+  int *g_occ = calloc(nn, sizeof(int));
+  const entry_t **eps = malloc(sizeof(entry_t *) * (stride + 1));
+  int *cand = malloc(sizeof(int) * (stride + 1));
+  int *best = malloc(sizeof(int) * (stride + 1));
+  double *buf = malloc(sizeof(double) * 5 * (stride + 1));
+  alloc_ws_t ws = {buf, buf + (stride + 1), buf + 2 * (stride + 1)};
+  int G = 0;
+  if (stats) stats[0] = stats[1] = 0;
+  for (int a = 0; a < n; ++a) {
+    gpu_of[a] = -1;
+    pos[a] = -1;
+    code[a] = 0;
+    int b = 0, need = 0;
+    igo_err e;
+    int rc = prologue_one(wl, ld, a, hw, b_max, cap, &b, &need, &e);
+    if (rc) {
+      code[a] = rc;
+      continue;
+    }
+    lbv[a] = need;
+    make_entry(&ents[a], wl, ld, a, b, hw);
+    int best_j = -1, best_inter = cap, best_n = 0;
+    for (int j = 0; j < G && !rc; ++j) {
+      int occupied = g_occ[j];
+      if (occupied + need > cap) continue;
+      if (stats) stats[1] += 1;
+      int nres = g_n[j] + 1;
+      for (int k = 0; k < nres - 1; ++k) {
+        eps[k] = &ents[g_res[(size_t)j * stride + k]];
+        cand[k] = g_units[(size_t)j * stride + k];
+      }
+      eps[nres - 1] = &ents[a];
+      cand[nres - 1] = need;
+      rc = alloc_units(eps, cand, nres, hw, cap, stats ? &stats[0] : NULL, &ws, &e);
+      if (rc) break;
+      int total = 0;
+      for (int k = 0; k < nres; ++k) total += cand[k];
+      if (total <= cap && total - occupied < best_inter) {
+        best_j = j;
+        best_inter = total - occupied;
+        best_n = nres;
+        memcpy(best, cand, sizeof(int) * nres);
+      }
+    }
+    if (rc) {
+      code[a] = rc;
+      continue;
+    }
+    if (best_j < 0) {
+      g_res[(size_t)G * stride] = a;
+      g_units[(size_t)G * stride] = need;
+      g_n[G] = 1;
+      g_occ[G] = need;
+      best_j = G++;
+    } else {
+      int occ = 0;
+      g_res[(size_t)best_j * stride + best_n - 1] = a;
+      for (int k = 0; k < best_n; ++k) {
+        g_units[(size_t)best_j * stride + k] = best[k];
+        occ += best[k];
+      }
+      g_n[best_j] = best_n;
+      g_occ[best_j] = occ;
+    }
+    gpu_of[a] = best_j;
+    pos[a] = g_n[best_j] - 1;
+  }
+  for (int a = 0; a < n; ++a) units_final[a] = 0;
+  for (int j = 0; j < G; ++j)
+    for (int k = 0; k < g_n[j]; ++k)
+      units_final[g_res[(size_t)j * stride + k]] = g_units[(size_t)j * stride + k];
+  if (gpu_count) *gpu_count = G;
+  free(ents); free(lbv); free(g_res); free(g_units); free(g_n); free(g_occ);
+  free(eps); free(cand); free(best); free(buf);
+  return 0;
+}

@@ -34,4 +34,7 @@ int igo_plan_batch(const double *wl, int n_scen, int m, const double *hw, int b_
                    int32_t *gpu_count, int64_t *stats, int n_threads);
 int igo_solo_grid(const double *wl, int64_t ld, int m, const double *hw, int b_max,
                   int32_t *min_units, int64_t *n_evals);
+int igo_stream(const double *wl, int64_t ld, int n, const double *hw, int b_max,
+               int32_t *gpu_of, int32_t *pos, int32_t *code, int32_t *units_final,
+               int32_t *gpu_count, int64_t *stats);
 #endif

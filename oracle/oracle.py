@@ -140,3 +140,21 @@ def solo_grid(wl, hw, b_max: int):
     lib().igo_solo_grid(_p(wl), ctypes.c_int64(m), ctypes.c_int(m), _p(hw), ctypes.c_int(b_max),
                         _p(out), _p(ev))
     return out, int(ev[0])
+
+
+def stream(wl, hw, b_max: int):
+    """Arrival-order provisioning (one planner.py:290-319 step per arrival,
+    rejected arrivals leave the state unchanged)."""
+    wl = np.ascontiguousarray(wl, np.float64)
+    n = wl.shape[1]
+    hw = np.ascontiguousarray(hw, np.float64)
+    gpu_of = np.zeros(n, np.int32)
+    pos = np.zeros(n, np.int32)
+    code = np.zeros(n, np.int32)
+    units = np.zeros(n, np.int32)
+    gc = np.zeros(1, np.int32)
+    st = np.zeros(2, np.int64)
+    lib().igo_stream(_p(wl), ctypes.c_int64(n), ctypes.c_int(n), _p(hw), ctypes.c_int(b_max),
+                     _p(gpu_of), _p(pos), _p(code), _p(units), _p(gc), _p(st))
+    return dict(gpu_of=gpu_of, pos=pos, code=code, units=units, gpu_count=int(gc[0]),
+                model_evals=int(st[0]), candidate_gpus=int(st[1]))

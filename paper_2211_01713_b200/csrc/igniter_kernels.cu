@@ -416,6 +416,11 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.S = n_scen;
   P.m = m;
   P.flags = flags;
+  P.k0 = 0;
+  P.k1 = m;
+  P.stream = 0;
+  P.code = nullptr;
+  P.sstate = nullptr;
   P.wl = wl;
   P.rank = name_rank;
   P.rank_stride = rank_stride;
@@ -590,6 +595,183 @@ int igp_prologue_device(const double *wl, int m, const double *hw_h, int b_max,
   k_prologue_err<<<1, 1, 0, st>>>(wl, m, hw, batch_in, fe, err);
   CK(cudaFreeAsync(fe, st));
   CK(cudaGetLastError());
+  return IGP_E_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Online stream (BASELINE config 5).  The workspace holds the plan workspace
+// for (n_streams, capacity) followed by the arrival tables and the
+// persistent per-stream state.
+// ---------------------------------------------------------------------------
+struct StreamLayout {
+  WsLayout L;
+  size_t wl, batch, lb, code, gpu_of, pos, units, pred, sstate, gc, err, total;
+};
+
+static StreamLayout stream_layout(int S, int C, int cap, int flags) {
+  StreamLayout X;
+  X.L = ws_layout(S, C, cap, flags);
+  const size_t SC = (size_t)S * (C > 0 ? C : 1);
+  size_t off = X.L.total;
+  X.wl = off; off = align_up(off + SC * IGP_WL_NF * 8);
+  X.batch = off; off = align_up(off + SC * 4);
+  X.lb = off; off = align_up(off + SC * 4);
+  X.code = off; off = align_up(off + SC * 4);
+  X.gpu_of = off; off = align_up(off + SC * 4);
+  X.pos = off; off = align_up(off + SC * 4);
+  X.units = off; off = align_up(off + SC * 4);
+  X.pred = off; off = align_up(off + SC * 80);
+  X.sstate = off; off = align_up(off + (size_t)S * 16);
+  X.gc = off; off = align_up(off + (size_t)S * 4);
+  X.err = off; off = align_up(off + (size_t)S * sizeof(igp_error));
+  X.total = off;
+  return X;
+}
+
+static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const Hw &hw, int S,
+                          int C, int flags) {
+  const WsLayout &L = X.L;
+  P.hw = hw;
+  P.S = S;
+  P.m = C;
+  P.flags = flags;
+  P.stream = 1;
+  P.wl = (const double *)(ws + X.wl);
+  P.rank = nullptr;
+  P.rank_stride = 0;
+  P.lanes = L.lanes;
+  P.gstride = L.gstride;
+  P.pool_recs = L.pool_recs;
+  P.by_rank = (int32_t *)(ws + L.by_rank);
+  P.order = (int32_t *)(ws + L.order);
+  P.cold = (double *)(ws + L.cold);
+  P.nw = (double *)(ws + L.nw);
+  P.tbl = (double *)(ws + L.tbl);
+  P.gstate = (unsigned long long *)(ws + L.gstate);
+  P.gcap = (int32_t *)(ws + L.gcap);
+  P.gfold = (double *)(ws + L.gfold);
+  P.rec = (double *)(ws + L.rec);
+  P.frec = (double *)(ws + L.frec);
+  P.pfx = (double *)(ws + L.pfx);
+  P.meta = (Meta *)(ws + L.meta);
+  P.lane_units = (uint16_t *)(ws + L.lane_units);
+  P.sflags = (int32_t *)(ws + L.sflags);
+  P.perr = (int32_t *)(ws + L.perr);
+  P.sched = (int32_t *)(ws + L.sched);
+  P.batch = (int32_t *)(ws + X.batch);
+  P.lb = (int32_t *)(ws + X.lb);
+  P.code = (int32_t *)(ws + X.code);
+  P.gpu_of = (int32_t *)(ws + X.gpu_of);
+  P.pos = (int32_t *)(ws + X.pos);
+  P.units = (int32_t *)(ws + X.units);
+  P.pred = nullptr;
+  P.sstate = (int32_t *)(ws + X.sstate);
+  P.gpu_count = (int32_t *)(ws + X.gc);
+  P.stats = nullptr;
+  P.err = (igp_error *)(ws + X.err);
+}
+
+size_t igp_stream_workspace_bytes(int n_streams, int capacity, const double *hw, int b_max,
+                                  int flags) {
+  Hw h = make_hw(hw, b_max);
+  return stream_layout(n_streams, capacity, h.cap, flags).total;
+}
+
+int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int b_max,
+                            void *workspace, size_t workspace_bytes, int flags, void *stream) {
+  if (n_streams < 1 || capacity < 1 || !hw_h || !workspace) return IGP_E_ARG;
+  Hw hw = make_hw(hw_h, b_max);
+  if (hw.cap < 1) return IGP_E_ARG;
+  if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
+  StreamLayout X = stream_layout(n_streams, capacity, hw.cap, flags);
+  if (workspace_bytes < X.total) return IGP_E_ARG;
+  CK(cudaMemsetAsync((char *)workspace + X.sstate, 0, (size_t)n_streams * 16,
+                     (cudaStream_t)stream));
+  return IGP_E_OK;
+}
+
+int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, int capacity,
+                           const double *hw_h, int b_max, int32_t *gpu_of, int32_t *pos,
+                           int32_t *code, int64_t *stats, void *workspace,
+                           size_t workspace_bytes, int flags, void *stream) {
+  if (n_streams < 1 || capacity < 1 || k0 < 0 || n < 0 || k0 + n > capacity || !hw_h ||
+      !workspace)
+    return IGP_E_ARG;
+  if (n == 0) return IGP_E_OK;
+  Hw hw = make_hw(hw_h, b_max);
+  if (hw.cap < 1) return IGP_E_ARG;
+  if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
+  StreamLayout X = stream_layout(n_streams, capacity, hw.cap, flags);
+  if (workspace_bytes < X.total) return IGP_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  char *ws = (char *)workspace;
+  const size_t S = (size_t)n_streams;
+  // append the arrivals: [S][16][n] -> columns [k0, k0 + n) of [S][16][capacity]
+  CK(cudaMemcpy2DAsync(ws + X.wl + (size_t)k0 * 8, (size_t)capacity * 8, wl_new, (size_t)n * 8,
+                       (size_t)n * 8, S * IGP_WL_NF, cudaMemcpyDeviceToDevice, st));
+  PlanParams P;
+  stream_params(P, X, ws, hw, n_streams, capacity, flags);
+  P.k0 = k0;
+  P.k1 = k0 + n;
+  P.stats = stats;
+  const long long tot = (long long)S * n;
+  k_prologue_plan<<<nblk(tot, 256), 256, 0, st>>>(P);
+  k_build<<<nblk(tot, 256), 256, 0, st>>>(P);
+  k_table<<<nblk(tot * TB, 256), 256, 0, st>>>(P);
+  if (hw.cap <= 48) launch_place<48>(P, st);
+  else if (hw.cap <= 128) launch_place<128>(P, st);
+  else launch_place<256>(P, st);
+  CK(cudaGetLastError());
+  const size_t dp = (size_t)capacity * 4, sp = (size_t)n * 4;
+  if (gpu_of)
+    CK(cudaMemcpy2DAsync(gpu_of, sp, ws + X.gpu_of + (size_t)k0 * 4, dp, sp, S,
+                         cudaMemcpyDeviceToDevice, st));
+  if (pos)
+    CK(cudaMemcpy2DAsync(pos, sp, ws + X.pos + (size_t)k0 * 4, dp, sp, S,
+                         cudaMemcpyDeviceToDevice, st));
+  if (code)
+    CK(cudaMemcpy2DAsync(code, sp, ws + X.code + (size_t)k0 * 4, dp, sp, S,
+                         cudaMemcpyDeviceToDevice, st));
+  return IGP_E_OK;
+}
+
+int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, const double *hw_h,
+                               int b_max, int32_t *gpu_of, int32_t *pos, int32_t *units,
+                               double *pred, int32_t *gpu_count, igp_error *err,
+                               void *workspace, size_t workspace_bytes, int flags,
+                               void *stream) {
+  if (n_streams < 1 || capacity < 1 || n_arrivals < 0 || n_arrivals > capacity || !hw_h ||
+      !workspace)
+    return IGP_E_ARG;
+  Hw hw = make_hw(hw_h, b_max);
+  if (hw.cap < 1) return IGP_E_ARG;
+  if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
+  StreamLayout X = stream_layout(n_streams, capacity, hw.cap, flags);
+  if (workspace_bytes < X.total) return IGP_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  char *ws = (char *)workspace;
+  const size_t S = (size_t)n_streams;
+  PlanParams P;
+  stream_params(P, X, ws, hw, n_streams, capacity, flags & ~IGP_F_NO_PRED);
+  P.k0 = P.k1 = n_arrivals;
+  P.pred = (double *)(ws + X.pred);
+  if (hw.cap <= 48) launch_place<48>(P, st);
+  else if (hw.cap <= 128) launch_place<128>(P, st);
+  else launch_place<256>(P, st);
+  CK(cudaGetLastError());
+  if (n_arrivals > 0) {
+    const size_t dp = (size_t)capacity * 4, sp = (size_t)n_arrivals * 4;
+    if (gpu_of)
+      CK(cudaMemcpy2DAsync(gpu_of, sp, ws + X.gpu_of, dp, sp, S, cudaMemcpyDeviceToDevice, st));
+    if (pos) CK(cudaMemcpy2DAsync(pos, sp, ws + X.pos, dp, sp, S, cudaMemcpyDeviceToDevice, st));
+    if (units)
+      CK(cudaMemcpy2DAsync(units, sp, ws + X.units, dp, sp, S, cudaMemcpyDeviceToDevice, st));
+    if (pred)
+      CK(cudaMemcpy2DAsync(pred, sp * 20, ws + X.pred, dp * 20, sp * 20, S,
+                           cudaMemcpyDeviceToDevice, st));
+  }
+  if (gpu_count) CK(cudaMemcpyAsync(gpu_count, ws + X.gc, S * 4, cudaMemcpyDeviceToDevice, st));
+  if (err) CK(cudaMemcpyAsync(err, ws + X.err, S * sizeof(igp_error), cudaMemcpyDeviceToDevice, st));
   return IGP_E_OK;
 }
 

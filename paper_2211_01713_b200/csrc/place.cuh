@@ -160,6 +160,14 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
 struct PlanParams {
   Hw hw;
   int S, m, flags;
+  // placement steps [k0, k1) of this launch.  Plan mode: [0, m), order from
+  // the (-lb, name) sort.  Stream mode (online arrivals, BASELINE config 5):
+  // placement order = arrival order, the per-scenario state (open GPUs, pool)
+  // persists across launches in sstate, and an arrival whose prologue or
+  // candidate evaluation raises is rejected instead of aborting the scenario.
+  int k0, k1, stream;
+  int32_t *code;    // stream: per arrival error code | risk flags << 8
+  int32_t *sstate;  // stream: per scenario {G, pool_top, sticky flags, arrivals}
   const double *wl;     // [S][16][m]
   const int32_t *rank;  // name ranks
   int rank_stride;
@@ -187,8 +195,9 @@ struct PlanParams {
 // thread per (scenario, workload): batch, lb, first-error key, risk flags, by_rank
 __global__ void k_prologue_plan(PlanParams P) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)P.S * P.m) return;
-  const int s = (int)(gid / P.m), i = (int)(gid % P.m);
+  const int span = P.k1 - P.k0;
+  if (gid >= (long long)P.S * span) return;
+  const int s = (int)(gid / span), i = P.k0 + (int)(gid % span);
   const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
   int b = -1, u = -1;
   double opnd;
@@ -196,11 +205,18 @@ __global__ void k_prologue_plan(PlanParams P) {
   const size_t o = (size_t)s * P.m + i;
   P.batch[o] = b;
   P.lb[o] = u;
-  const int32_t *rk = P.rank + (size_t)s * P.rank_stride;
-  P.by_rank[(size_t)s * P.m + rk[i]] = i;
-  if (rc) {
-    atomicMin(&P.perr[s], i);  // first error in INPUT order (planner.py:280-282)
-    return;
+  if (P.stream) {
+    if (rc) {  // the arrival is rejected
+      P.code[o] = rc;
+      return;
+    }
+  } else {
+    const int32_t *rk = P.rank + (size_t)s * P.rank_stride;
+    P.by_rank[(size_t)s * P.m + rk[i]] = i;
+    if (rc) {
+      atomicMin(&P.perr[s], i);  // first error in INPUT order (planner.py:280-282)
+      return;
+    }
   }
   // NonPositiveDenominatorError screen: denom(u) = u*r_unit + k4 is
   // non-decreasing in u and k_act(u) = gamma/denom(u) + k5 is monotone in u
@@ -218,7 +234,8 @@ __global__ void k_prologue_plan(PlanParams P) {
       !isfinite(slot[S_TLOAD] + slot[S_TFB] + slot[S_THALF] + cold[C_KSCH] * cold[C_NK]))
     fl |= SF_NO_MARGIN;
   if (!(u <= 0xffff)) fl |= SF_RISKY;
-  if (fl) atomicOr(&P.sflags[s], fl);
+  if (P.stream) P.code[o] = fl << 8;
+  else if (fl) atomicOr(&P.sflags[s], fl);
 }
 
 // warp per scenario: stable counting sort by (-lb, name rank) (planner.py:284)
@@ -267,11 +284,12 @@ __global__ void k_sort(PlanParams P) {
 // thread per (scenario, placement position k): cold constants + newcomer record
 __global__ void k_build(PlanParams P) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)P.S * P.m) return;
-  const int s = (int)(gid / P.m), k = (int)(gid % P.m);
-  if (P.perr[s] != INT_MAX) return;
+  const int span = P.k1 - P.k0;
+  if (gid >= (long long)P.S * span) return;
+  const int s = (int)(gid / span), k = P.k0 + (int)(gid % span);
   const size_t sm = (size_t)s * P.m;
-  const int i = P.order[sm + k];
+  if (P.stream ? (P.code[sm + k] & 0xff) != 0 : P.perr[s] != INT_MAX) return;
+  const int i = P.stream ? k : P.order[sm + k];
   const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
   double cold[C_NF], slot[S_NF];
   const int b = P.batch[sm + i], u = P.lb[sm + i];
@@ -296,14 +314,16 @@ __global__ void k_build(PlanParams P) {
 // thread per (scenario, k, v): solo table entry at u = lb + v (model.py:285-297)
 __global__ void k_table(PlanParams P) {
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)P.S * P.m * TB) return;
-  const long long sk = gid / TB;
+  const int span = P.k1 - P.k0;
+  if (gid >= (long long)P.S * span * TB) return;
+  const long long lk = gid / TB;
   const int v = (int)(gid % TB);
-  const int s = (int)(sk / P.m);
-  if (P.perr[s] != INT_MAX) return;
+  const int s = (int)(lk / span);
+  const long long sk = (long long)s * P.m + P.k0 + (lk % span);
+  if (P.stream ? (P.code[sk] & 0xff) != 0 : P.perr[s] != INT_MAX) return;
   const double *cd = P.cold + sk * C_NF;
   const int u = (int)cd[C_LB] + v;
-  double *t = P.tbl + gid * 4;
+  double *t = P.tbl + (sk * TB + v) * 4;
   if (u > P.hw.cap) {
     t[0] = t[1] = t[2] = t[3] = 0.0;
     return;
@@ -443,7 +463,7 @@ k_place(PlanParams P) {
   const size_t sm = (size_t)s * m;
   igp_error *err = P.err + s;
 
-  if (P.perr[s] != INT_MAX) {  // prologue error, input order (planner.py:280-282)
+  if (!P.stream && P.perr[s] != INT_MAX) {  // prologue error, input order (planner.py:280-282)
     if (t == 0) {
       const int i = P.perr[s];
       int b, u;
@@ -480,14 +500,14 @@ k_place(PlanParams P) {
   double *pfx = P.pfx + sp * 4;
   Meta *meta = P.meta + sp;
   uint16_t *lane_units = P.lane_units + (size_t)s * P.lanes * cap;
-  const int sflags = P.sflags[s];
-  const bool exact = (P.flags & IGP_F_STATS) || (sflags & SF_RISKY);
-  const bool margin = !(sflags & SF_NO_MARGIN) && hw.margin_ok;
+  int32_t *sst = P.stream ? P.sstate + 4 * (size_t)s : nullptr;
+  // stream mode: risk flags of admitted arrivals stick to the scenario
+  int sflags = P.stream ? sst[2] : P.sflags[s];
   const unsigned lt = (1u << lane) - 1u;
 
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
-  int G = 0;
+  int G = P.stream ? sst[0] : 0;
   long long tot_evals = 0, tot_calls = 0, tot_cands = 0;
   long long st_evals = 0, st_calls = 0, st_cands = 0;
   int fail_code = 0;
@@ -495,11 +515,27 @@ k_place(PlanParams P) {
   eo_fail.code = 0;
   eo_fail.k = -1;
   if (t == 0) {
-    gs.pool_top = 0;
+    gs.pool_top = P.stream ? sst[1] : 0;
     gs.abort_code = 0;
   }
+  group_sync<GW>();
 
-  for (int k = 0; k < m; ++k) {
+  for (int k = P.k0; k < P.k1; ++k) {
+    int aflags = 0;  // this arrival's risk flags (stream mode)
+    if (P.stream) {
+      const int c = P.code[sm + k];
+      if (c & 0xff) {  // rejected by the prologue
+        if (t == 0) {
+          P.gpu_of[sm + k] = -1;
+          P.pos[sm + k] = -1;
+          P.units[sm + k] = 0;
+        }
+        continue;
+      }
+      aflags = c >> 8;
+    }
+    const bool exact = (P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY);
+    const bool margin = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
     // the newcomer (planner.py:291-292)
     const double *ck = cold + (size_t)k * C_NF;
     const double *nk_rec = nwt + (size_t)k * R_NF;
@@ -514,7 +550,7 @@ k_place(PlanParams P) {
       gs.err_flag = 0;
     }
     for (int x = t; x < TB * 4; x += GT) ntab[x] = tbl[(size_t)k * TB * 4 + x];
-    if (t == 0 && k + 1 < m) {  // the next newcomer's rows
+    if (t == 0 && k + 1 < P.k1) {  // the next newcomer's rows
       prefetch_l2(cold + (size_t)(k + 1) * C_NF, C_NF * 8);
       prefetch_l2(nwt + (size_t)(k + 1) * R_NF, R_NF * 8);
       prefetch_l2(tbl + (size_t)(k + 1) * TB * 4, TB * 32);
@@ -919,6 +955,17 @@ k_place(PlanParams P) {
       tot_evals += st_evals;
       tot_calls += st_calls;
       tot_cands += st_cands;
+      if (P.stream) {  // the arrival is rejected; the state is unchanged
+        if (t == 0) {
+          P.code[sm + k] = eo_fail.code | (aflags << 8);
+          P.gpu_of[sm + k] = -1;
+          P.pos[sm + k] = -1;
+          P.units[sm + k] = 0;
+        }
+        st_evals = st_calls = st_cands = 0;
+        group_sync<GW>();
+        continue;
+      }
       fail_code = 1;
       break;
     }
@@ -970,6 +1017,10 @@ k_place(PlanParams P) {
             gf[1] = fp.c;
             gf[2] = fc.s;
             gf[3] = fc.c;
+            if (P.stream) {
+              P.gpu_of[sm + k] = G;
+              P.pos[sm + k] = 0;
+            }
           }
         }
       } else {
@@ -1070,11 +1121,16 @@ k_place(PlanParams P) {
             gf[1] = fp.c;
             gf[2] = fc.s;
             gf[3] = fc.c;
+            if (P.stream) {
+              P.gpu_of[sm + k] = j;
+              P.pos[sm + k] = nres;
+            }
           }
         }
       }
     }
     if (bk == NO_KEY) G += 1;
+    sflags |= aflags;  // an admitted risky arrival can raise in later steps
     if (wi == 0) fence_async_global();  // commit writes -> next step's tile copies
     __threadfence_block();
     group_sync<GW>();
@@ -1097,6 +1153,24 @@ k_place(PlanParams P) {
     P.stats[4 * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
     P.stats[4 * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
     P.stats[4 * s + 3] = (long long)gs.tot[1];
+  }
+
+  if (P.stream && t == 0) {  // persist the scenario state for the next push
+    sst[0] = G;
+    sst[1] = gs.pool_top;
+    sst[2] = sflags;
+    sst[3] = P.k1;
+  }
+  if (P.stream && !P.pred && !fail_code) {
+    if (t == 0) {
+      err->code = 0;
+      err->workload = -1;
+      err->gpu = -1;
+      err->a = err->b = err->c = 0.0;
+      P.gpu_count[s] = G;
+    }
+    group_sync<GW>();
+    continue;
   }
 
   if (fail_code) {

@@ -307,8 +307,66 @@ def grid_case(workloads, hw, b_max):
     return out
 
 
+def stream_reference(workloads, hw, b_max=32):
+    """Online arrival-order provisioning over the reference's own internals
+    (no reference API exists, plan() always sorts).  Each
+    arrival is one step of planner.py:290-319 against the persistent state,
+    with the batch and lower bound of planner.py:280-282; an arrival whose
+    prologue or candidate evaluation raises is rejected and leaves the state
+    unchanged.  Returns per-arrival GPU, position and error code, plus the
+    final units of every admitted arrival."""
+    cap = gplanner.max_units(hw)
+    names, entries, units = [], [], []
+    n = len(workloads)
+    gpu_of = np.full(n, -1, np.int32)
+    pos = np.full(n, -1, np.int32)
+    code = np.zeros(n, np.int32)
+    where = {}
+    for a, (spec, coef) in enumerate(workloads):
+        try:
+            b = gp.appropriate_batch(spec, hw, b_max)
+            need = gplanner._lower_bound_units(spec, coef, hw, b)
+        except gerr.PlanningError as exc:
+            code[a] = err_code(exc)
+            continue
+        entry = gmodel._Entry(spec, coef, b, hw)
+        best_j, best_inter, best_units = -1, cap, None
+        try:
+            for j in range(len(names)):
+                occupied = sum(units[j])
+                if occupied + need > cap:
+                    continue
+                cand = gplanner._alloc_units(entries[j] + [entry], units[j] + [need], hw, cap)
+                total = sum(cand)
+                if total <= cap and total - occupied < best_inter:
+                    best_j, best_inter, best_units = j, total - occupied, cand
+        except gerr.NonPositiveDenominatorError as exc:
+            code[a] = err_code(exc)
+            continue
+        if best_j < 0:
+            names.append([a]); entries.append([entry]); units.append([need])
+            best_j = len(names) - 1
+        else:
+            names[best_j].append(a); entries[best_j].append(entry); units[best_j] = list(best_units)
+        gpu_of[a] = best_j
+        pos[a] = len(names[best_j]) - 1
+    final_units = np.zeros(n, np.int32)
+    for j, mem in enumerate(names):
+        for k, a in enumerate(mem):
+            final_units[a] = units[j][k]
+    return gpu_of, pos, code, final_units
+
+
+def stream_case(workloads, hw, b_max=32):
+    out = pack_instance(workloads, hw, b_max)
+    gpu_of, pos, code, units = stream_reference(workloads, hw, b_max)
+    out.update(gpu_of=gpu_of, pos=pos, code=code, units=units,
+               gpu_count=np.int64(gpu_of.max() + 1 if (gpu_of >= 0).any() else 0))
+    return out
+
+
 def main():
-    groups = set(sys.argv[1:]) or {"plan", "component", "grid"}
+    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream"}
     mpath = os.path.join(HERE, "manifest.json")
     manifest = json.load(open(mpath))["cases"] if os.path.exists(mpath) else {}
     v100 = support.make_v100()
@@ -414,6 +472,20 @@ def main():
         save("grid_edge_30", grid_case(odd, v100, 48),
              "solo grid edge cases: denominator / active-time errors, f_min floor, "
              "infeasible everywhere, wide coefficients")
+
+    # ---- online stream (BASELINE config 5): arrival order, no sort ---------
+    if "stream" in groups:
+        save("stream_c2_600", stream_case(support.random_instance(np.random.default_rng(505), 600, v100),
+                                          v100), "stream: 600 random_instance arrivals in arrival order")
+        save("stream_r01_300", stream_case(support.random_instance(np.random.default_rng(506), 300, hw01),
+                                           hw01), "stream: 300 arrivals, r_unit 0.01 (cap 100)")
+        inst = support.random_instance(np.random.default_rng(507), 120, v100)
+        mix = (inst[:20] + [(gp.WorkloadSpec("s_slo", 0.9, 100.0, 0.574, 0.004), support.demo_coef())]
+               + inst[20:40] + [(gp.WorkloadSpec("s_cap", 200.0, 2000.0, 0.0, 0.0), support.demo_coef())]
+               + inst[40:60] + [denom_error_workload("s_neg", -0.5)] + inst[60:80]
+               + [denom_error_workload("s_negk", 0.05, k3=-3.0)] + inst[80:])
+        save("stream_errors_124", stream_case(mix, v100),
+             "stream with rejected arrivals: infeasible SLO, batch cap, r + k4 <= 0, k_act <= 0")
 
     # ---- component cases ------------------------------------------------
     if "component" not in groups:

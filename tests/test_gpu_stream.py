@@ -1,0 +1,85 @@
+"""Online stream (BASELINE config 5) on the GPU vs the reference-internals
+driver (golden fixtures, make_golden.py stream_reference) and the CPU oracle."""
+import numpy as np
+import pytest
+
+import golden_io as G
+
+from paper_2211_01713_b200 import synth
+from paper_2211_01713_b200.layout import hw_vector
+from paper_2211_01713_b200.stream import StreamPlanner
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _hw(d):
+    from instances import hw_from_golden
+    return hw_from_golden(d)
+
+
+def _push_in_chunks(sp, wl, chunks):
+    out = {k: [] for k in ("gpu_of", "pos", "code")}
+    k = 0
+    for c in chunks:
+        r = sp.push_arrays(wl[:, :, k:k + c])
+        for key in out:
+            out[key].append(r[key])
+        k += c
+    return {key: np.concatenate(v, axis=1) for key, v in out.items()}
+
+
+@pytest.mark.parametrize("case", G.names("stream_"))
+@pytest.mark.parametrize("chunks", ["one", "ragged"])
+def test_stream_matches_reference_driver(case, chunks):
+    d = G.load(case)
+    n = d["wl"].shape[1]
+    sizes = [n] if chunks == "one" else [1, 7, 64, 3, n - 75] if n > 80 else [n]
+    sp = StreamPlanner(_hw(d), capacity=n, b_max=int(d["b_max"]))
+    r = _push_in_chunks(sp, d["wl"][None], sizes)
+    np.testing.assert_array_equal(r["gpu_of"][0], d["gpu_of"])
+    np.testing.assert_array_equal(r["pos"][0], d["pos"])
+    np.testing.assert_array_equal(r["code"][0], d["code"])
+    snap = sp.snapshot()
+    np.testing.assert_array_equal(snap["units"][0], d["units"])
+    np.testing.assert_array_equal(snap["gpu_of"][0], d["gpu_of"])
+    assert int(snap["gpu_count"][0]) == int(d["gpu_count"])
+
+
+def test_many_streams_vs_oracle(oracle_lib):
+    from instances import make_v100
+    hw = make_v100()
+    S, n = 6, 1500
+    wl, _ = synth.scenarios(S, n, hw, seed=77)
+    sp = StreamPlanner(hw, capacity=n, n_streams=S)
+    r = _push_in_chunks(sp, wl, [100] * 15)
+    snap = sp.snapshot(with_predictions=True)
+    for s in range(S):
+        o = oracle_lib.stream(wl[s], np.array(hw_vector(hw)), 32)
+        np.testing.assert_array_equal(r["gpu_of"][s], o["gpu_of"])
+        np.testing.assert_array_equal(r["pos"][s], o["pos"])
+        np.testing.assert_array_equal(r["code"][s], o["code"])
+        np.testing.assert_array_equal(snap["units"][s], o["units"])
+        assert int(snap["gpu_count"][s]) == o["gpu_count"]
+        assert int(snap["err"][s]["code"]) == 0
+        assert np.isfinite(snap["pred"][s]).all()
+
+
+def test_stream_r_unit_001_b128_vs_oracle(oracle_lib):
+    from instances import make_v100
+    hw = make_v100(r_unit=0.01)
+    S, n = 3, 800
+    wl, _ = synth.scenarios(S, n, hw, seed=78, slo=(20.0, 100.0), rate=(50.0, 6000.0), b_max=128)
+    sp = StreamPlanner(hw, capacity=n, n_streams=S, b_max=128)
+    r = _push_in_chunks(sp, wl, [200, 200, 400])
+    snap = sp.snapshot()
+    for s in range(S):
+        o = oracle_lib.stream(wl[s], np.array(hw_vector(hw)), 128)
+        np.testing.assert_array_equal(r["gpu_of"][s], o["gpu_of"])
+        np.testing.assert_array_equal(snap["units"][s], o["units"])

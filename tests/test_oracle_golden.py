@@ -90,3 +90,13 @@ def test_oracle_solo_grid_matches_reference(oracle_lib, case):
     mu, evals = oracle_lib.solo_grid(d["wl"], d["hw"], int(d["b_max"]))
     np.testing.assert_array_equal(mu, d["min_units"])
     assert evals > 0
+
+
+@pytest.mark.parametrize("case", G.names("stream_"))
+def test_oracle_stream_matches_reference_driver(oracle_lib, case):
+    """Arrival-order stream vs the reference-internals driver (make_golden.py)."""
+    d = G.load(case)
+    o = oracle_lib.stream(d["wl"], d["hw"], int(d["b_max"]))
+    for k in ("gpu_of", "pos", "code", "units"):
+        np.testing.assert_array_equal(o[k], d[k], err_msg=k)
+    assert o["gpu_count"] == int(d["gpu_count"])
