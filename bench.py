@@ -41,6 +41,13 @@ V100 = dict(gpu_type="v100", power_max_w=300.0, freq_max_mhz=1530.0, power_idle_
             beta_sch_ms=-0.00902, r_unit=0.025, price_per_hour=3.06)
 FLOPS_PER_MODEL_EVAL = 30   # fp64 ops per resident evaluation
 FLOPS_PER_EVAL_CALL = 9     # fp64 ops per device evaluation
+# a (workload, GPU) trial reads the candidate
+# GPU's resident state once -- 8 fp64 terms per resident (k_act, cache, t_sch,
+# alpha_cache, t_load, t_feedback, t_half, power) -- plus the GPU descriptor
+# and its two Neumaier fold states (8 + 32 B)
+BYTES_PER_RESIDENT_READ = 64
+BYTES_PER_TRIAL = 40
+KERNELS_PER_PLAN_CALL = 6   # k_fill_int, k_prologue_plan, k_sort, k_build, k_table, k_place
 
 
 def parse():
@@ -56,6 +63,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--flags", type=int, default=0, help="extra IGP_F_* flags")
+    ap.add_argument("--ncu-traffic", type=float, default=None,
+                    help="dram bytes per k_place launch from an ncu --set full capture of "
+                         "this configuration (profiles/), reported as roofline.traffic")
     return ap.parse_args()
 
 
@@ -127,6 +137,24 @@ class ClockSampler:
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons,
                 "samples": len(rows)}
+
+
+def ncu_traffic(S, m):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_place launch at
+    this configuration, from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(f"k_place S={S} m={m}", {}).get("dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}
 
 
 def fp64_peak():
@@ -232,7 +260,7 @@ def main():
     i32 = torch.empty((5, S, m), dtype=torch.int32, device=device)
     d_pred = torch.empty((S, m, 10), dtype=torch.float64, device=device)
     d_gc = torch.empty(S, dtype=torch.int32, device=device)
-    d_st = torch.empty((S, 4), dtype=torch.int64, device=device)
+    d_st = torch.empty((S, 6), dtype=torch.int64, device=device)
     d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
     ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, b_max, flags | IGP_F_STATS),
                      dtype=torch.uint8, device=device)
@@ -254,14 +282,15 @@ def main():
     ref_model_evals = int(st[:, 0].sum())
     ref_cands = int(st[:, 1].sum())
     ref_calls = int(st[:, 2].sum())
+    ref_res_reads = int(st[:, 4].sum())
     gpus_exact = d_gc.cpu().numpy().copy()
     units_exact = i32[2].cpu().numpy().copy()
 
-    # gather buffers for N>1: fixed-size records (gpu_of + units per workload, gpu_count)
+    # N>1: the fixed-size plan records (GPU index + units per workload, GPU
+    # count) of every rank's shard are all-gathered over NCCL inside the step
     if world > 1:
         import torch.distributed as dist
-        rec = torch.empty((S, 2 * m + 1), dtype=torch.int32, device=device)
-        gathered = torch.empty((world, S, 2 * m + 1), dtype=torch.int32, device=device)
+        from paper_2211_01713_b200 import shard
 
     def step(ev=None):
         if ev is not None:
@@ -273,10 +302,7 @@ def main():
         if ev is not None:
             ev[2].record(stream)
         if world > 1:
-            rec[:, :m].copy_(i32[0])
-            rec[:, m:2 * m].copy_(i32[2])
-            rec[:, 2 * m].copy_(d_gc)
-            dist.all_gather_into_tensor(gathered.view(-1), rec.view(-1))
+            shard.gather_records(shard.pack_records(i32[0], i32[2], d_gc), S * world, world)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -319,7 +345,7 @@ def main():
         out = {k: torch.empty((S, m), dtype=torch.int32).pin_memory().numpy()
                for k in ("gpu_of", "pos", "units", "batch", "lb")}
         out["gpu_count"] = torch.empty(S, dtype=torch.int32).pin_memory().numpy()
-        out["stats"] = torch.empty((S, 4), dtype=torch.int64).pin_memory().numpy()
+        out["stats"] = torch.empty((S, 6), dtype=torch.int64).pin_memory().numpy()
         out["err"] = np.zeros(S, _native.err_dtype())
         del ws
         torch.cuda.empty_cache()
@@ -347,23 +373,39 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e2e_ms / args.steps}
 
-    # ---- roofline of the dominant kernel (k_plan, the place stage) ----
+    # ---- roofline of the dominant kernel (k_place, the place stage) ----
+    # Both rooflines count the REFERENCE's work (exact-stats pass), not the
+    # smaller amount the pruned fast path performs.
     place_avg = sum(place_ms) / len(place_ms)
-    flops_per_launch = FLOPS_PER_MODEL_EVAL * ref_model_evals + FLOPS_PER_EVAL_CALL * ref_calls
-    peak_fma, peak_add = fp64_peak()
-    achieved = flops_per_launch / (place_avg / 1e3) / 1e12
+    bytes_per_launch = BYTES_PER_RESIDENT_READ * ref_res_reads + BYTES_PER_TRIAL * ref_cands
+    achieved_gbs = bytes_per_launch / (place_avg / 1e3) / 1e9
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
     roofline = {
-        "bound": "fp64", "achieved": achieved,
-        "peak": (peak_fma / 1e12) if peak_fma else None, "unit": "TFLOP/s",
-        "frac": (achieved / (peak_fma / 1e12)) if peak_fma else None,
-        "traffic": None,
-        "kernel": "k_plan (igp_plan_place_device)",
-        "peak_source": "measured DFMA rate, tools/fp64_probe.cu (MEASURED_PEAKS.json has no FP64 figure)",
-        "peak_dadd_tflops": (peak_add / 1e12) if peak_add else None,
-        "flops_definition": f"{FLOPS_PER_MODEL_EVAL} x reference model_evals + "
-                            f"{FLOPS_PER_EVAL_CALL} x reference _eval_entries calls per launch",
+        "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+        "frac": achieved_gbs / hbm_peak if hbm_peak else None,
+        "traffic": args.ncu_traffic if args.ncu_traffic is not None else ncu_traffic(S, m),
+        "kernel": "k_place (igp_plan_place_device)",
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth, burst)"
+                       if "hbm_gbs" in peaks else "fallback 6650 GB/s (B200_PROFILING.md)",
+        "bytes_definition": f"{BYTES_PER_RESIDENT_READ} B x reference resident reads "
+                            f"({ref_res_reads}) + {BYTES_PER_TRIAL} B x reference candidate "
+                            f"trials ({ref_cands}) per launch",
+        "bytes_per_launch": bytes_per_launch,
         "place_ms_avg": place_avg, "prepare_ms_avg": sum(prep_ms) / len(prep_ms),
         "place_share_of_step": place_avg / (ms_total / args.steps) if world == 1 else None,
+    }
+    flops_per_launch = FLOPS_PER_MODEL_EVAL * ref_model_evals + FLOPS_PER_EVAL_CALL * ref_calls
+    peak_fma, peak_add = fp64_peak()
+    achieved_tf = flops_per_launch / (place_avg / 1e3) / 1e12
+    roofline_fp64 = {
+        "bound": "fp64", "achieved": achieved_tf,
+        "peak": (peak_fma / 1e12) if peak_fma else None, "unit": "TFLOP/s",
+        "frac": (achieved_tf / (peak_fma / 1e12)) if peak_fma else None,
+        "peak_source": "measured DFMA rate on this GPU, tools/fp64_probe.cu "
+                       "(MEASURED_PEAKS.json has no FP64 figure)",
+        "flops_definition": f"{FLOPS_PER_MODEL_EVAL} x reference model_evals + "
+                            f"{FLOPS_PER_EVAL_CALL} x reference _eval_entries calls per launch",
     }
 
     cpu = None
@@ -394,10 +436,12 @@ def main():
             "reference_counters_per_gpu_step": {"model_evals": ref_model_evals,
                                                 "candidate_gpus": ref_cands,
                                                 "eval_calls": ref_calls,
+                                                "resident_reads": ref_res_reads,
                                                 "eval_calls_run_fast_path": performed_calls},
-            "gpu_launches": 5 * args.steps * (1 if args.no_e2e else 2),
+            "gpu_launches": KERNELS_PER_PLAN_CALL * args.steps * (1 if args.no_e2e else 2),
             "clocks": clocks,
             "roofline": roofline,
+            "roofline_fp64": roofline_fp64,
             "cpu_baseline": cpu,
             "e2e": e2e,
         }

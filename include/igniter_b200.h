@@ -94,6 +94,8 @@ typedef struct igp_error {
   double a, b, c;   /* message operands, see the enum above */
 } igp_error;
 
+#define IGP_NSTAT 6 /* int64 counters per scenario in the stats outputs */
+
 /* plan flags */
 enum {
   IGP_F_STATS = 1,      /* exact PlanStats (model_evals, candidate_gpus) for every
@@ -124,11 +126,13 @@ size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, 
  *                                   lower-bound units)
  *   pred        [S][m][10] fp64 breakdown rows (NULL or IGP_F_NO_PRED: skipped)
  *   gpu_count   [S]
- *   stats       [S][4] int64 {model_evals, candidate_gpus, eval_calls, evals_run}:
- *               the reference's PlanStats counters (planner.py:64-69) and its
- *               number of _eval_entries calls -- exact with IGP_F_STATS (or for
- *               a scenario that raised), -1 otherwise -- and the number of
- *               device evaluations this kernel actually ran
+ *   stats       [S][IGP_NSTAT] int64 {model_evals, candidate_gpus, eval_calls,
+ *               evals_run, resident_reads, candidates_run}: the reference's
+ *               PlanStats counters (planner.py:64-69), its number of
+ *               _eval_entries calls and the residents its candidate trials read
+ *               (sum over trials of the GPU's resident count) -- exact with
+ *               IGP_F_STATS (or for a scenario that raised), -1 otherwise --
+ *               and the device evaluations / candidates this kernel actually ran
  *   err         [S] igp_error
  * returns IGP_E_OK or the first error code over scenarios (per-scenario codes
  * are in err[s].code).

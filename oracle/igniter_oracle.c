@@ -315,10 +315,10 @@ static int cmp_order(const void *a, const void *b) {
 int igo_plan(const double *wl, int64_t ld, int m, const double *hw, int b_max,
              const int32_t *name_rank, int32_t *gpu_of, int32_t *pos, int32_t *units_out,
              int32_t *batch_out, int32_t *lb_out, double *pred, int32_t *gpu_count,
-             int64_t *stats /* [model_evals, candidate_gpus] */, igo_err *err) {
+             int64_t *stats /* [model_evals, candidate_gpus, resident_reads] */, igo_err *err) {
   int cap = igo_max_units(hw);
   if (err) memset(err, 0, sizeof(*err));
-  if (stats) stats[0] = stats[1] = 0;
+  if (stats) stats[0] = stats[1] = stats[2] = 0;
   /* prologue in input order: planner.py:280-282 (batch before lb per workload) */
   for (int i = 0; i < m; ++i) {
     int b = 0, u = 0;
@@ -357,7 +357,10 @@ int igo_plan(const double *wl, int64_t ld, int m, const double *hw, int b_max,
     for (int j = 0; j < G; ++j) {
       int occupied = g_occ[j];
       if (occupied + need > cap) continue;
-      if (stats) stats[1] += 1;
+      if (stats) {
+        stats[1] += 1;
+        stats[2] += g_n[j];
+      }
       int n = g_n[j] + 1;
       for (int k = 0; k < n - 1; ++k) {
         eps[k] = &ents[g_res[(size_t)j * stride + k]];
@@ -464,7 +467,7 @@ static void *batch_worker(void *arg) {
     int rc = igo_plan(j->wl + (int64_t)s * j->scen_stride, m, m, j->hw, j->b_max,
                       j->name_rank, j->gpu_of + (int64_t)s * m, pos,
                       j->units + (int64_t)s * m, bt, lb, NULL, j->gpu_count + s,
-                      j->stats ? j->stats + 2 * s : NULL, &e);
+                      j->stats ? j->stats + 3 * s : NULL, &e);
     if (rc && !j->rc) j->rc = rc;
   }
   free(pos);

@@ -62,14 +62,14 @@ def plan(wl: np.ndarray, hw, b_max: int, rank: np.ndarray):
     out = {k: np.full(m, -1, np.int32) for k in ("gpu_of", "pos", "units", "batch", "lb")}
     pred = np.zeros((m, 10))
     gc = np.zeros(1, np.int32)
-    stats = np.zeros(2, np.int64)
+    stats = np.zeros(3, np.int64)
     err = IgoErr()
     rc = lib().igo_plan(_p(wl), ctypes.c_int64(m), ctypes.c_int(m), _p(hw), ctypes.c_int(b_max),
                         _p(rank), _p(out["gpu_of"]), _p(out["pos"]), _p(out["units"]),
                         _p(out["batch"]), _p(out["lb"]), _p(pred), _p(gc), _p(stats),
                         ctypes.byref(err))
     out.update(pred=pred, gpu_count=int(gc[0]), model_evals=int(stats[0]),
-               candidate_gpus=int(stats[1]), rc=int(rc),
+               candidate_gpus=int(stats[1]), resident_reads=int(stats[2]), rc=int(rc),
                err=(err.code, err.workload, err.a, err.b, err.c))
     return out
 
@@ -83,7 +83,7 @@ def plan_batch(wl: np.ndarray, hw, b_max: int, rank: np.ndarray, threads: int, s
     gpu_of = np.zeros((S, m), np.int32)
     units = np.zeros((S, m), np.int32)
     gc = np.zeros(S, np.int32)
-    st = np.zeros((S, 2), np.int64) if stats else None
+    st = np.zeros((S, 3), np.int64) if stats else None
     rc = lib().igo_plan_batch(_p(wl), ctypes.c_int(S), ctypes.c_int(m), _p(hw), ctypes.c_int(b_max),
                               _p(rank), _p(gpu_of), _p(units), _p(gc),
                               _p(st) if stats else None, ctypes.c_int(threads))

@@ -115,7 +115,7 @@ def _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred):
         i32 = torch.empty((5, S, max(m, 1)), dtype=torch.int32, device=device)
         d_pred = torch.empty((S, max(m, 1), 10), dtype=torch.float64, device=device) if want_pred else None
         d_gc = torch.empty(S, dtype=torch.int32, device=device)
-        d_st = torch.empty((S, 4), dtype=torch.int64, device=device)
+        d_st = torch.empty((S, 6), dtype=torch.int64, device=device)
         d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
         nbytes = plan_workspace_bytes(S, m, h, b_max, flags)
         ws = workspace(nbytes, device)
@@ -149,7 +149,7 @@ def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=False, ou
         out = dict(gpu_of=np.empty((S, m), np.int32), pos=np.empty((S, m), np.int32),
                    units=np.empty((S, m), np.int32), batch=np.empty((S, m), np.int32),
                    lb=np.empty((S, m), np.int32), gpu_count=np.empty(S, np.int32),
-                   stats=np.empty((S, 4), np.int64),
+                   stats=np.empty((S, 6), np.int64),
                    err=np.zeros(S, _native.err_dtype()))
         if want_pred:
             out["pred"] = np.empty((S, m, 10))
@@ -175,7 +175,7 @@ def host_workspace_bytes(S, m, hw_vec, b_max, flags, rank_stride, want_pred):
     def al(x):
         return (x + 255) & ~255
     extra = al(Sm * WL_NF * 8) + al((Sm if rank_stride else max(m, 1)) * 4) + al(Sm * 20)
-    extra += al(Sm * 80 if want_pred else 0) + al(S * 4) + al(S * 32)
+    extra += al(Sm * 80 if want_pred else 0) + al(S * 4) + al(S * 48)
     extra += al(S * ctypes.sizeof(_native.IgpError))
     return base + extra + 4096
 

@@ -505,7 +505,7 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
   size_t o_i32 = off; off = align_up(off + Sm * 4 * 5);
   size_t o_pred = off; off = align_up(off + (pred ? Sm * 80 : 0));
   size_t o_gc = off; off = align_up(off + (size_t)n_scen * 4);
-  size_t o_st = off; off = align_up(off + (size_t)n_scen * 32);
+  size_t o_st = off; off = align_up(off + (size_t)n_scen * 8 * IGP_NSTAT);
   size_t o_err = off; off = align_up(off + (size_t)n_scen * sizeof(igp_error));
   if (!workspace || workspace_bytes < off) return IGP_E_ARG;
   char *ws = (char *)workspace;
@@ -535,7 +535,8 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
     if (pred) CK(cudaMemcpyAsync(pred, d_pred, Sm * 80, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaMemcpyAsync(gpu_count, d_gc, (size_t)n_scen * 4, cudaMemcpyDeviceToHost, st));
-  if (stats) CK(cudaMemcpyAsync(stats, d_st, (size_t)n_scen * 32, cudaMemcpyDeviceToHost, st));
+  if (stats)
+    CK(cudaMemcpyAsync(stats, d_st, (size_t)n_scen * 8 * IGP_NSTAT, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(err, d_err, (size_t)n_scen * sizeof(igp_error), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int s = 0; s < n_scen; ++s)

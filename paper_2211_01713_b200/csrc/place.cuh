@@ -340,7 +340,7 @@ __global__ void k_table(PlanParams P) {
 // ---------------------------------------------------------------------------
 struct GroupSmem {
   unsigned long long best;
-  unsigned long long tot[3];  // model_evals, eval calls, candidates
+  unsigned long long tot[5];  // model_evals, eval calls, candidates, resident reads, started
   int err_flag;
   int win_thread;
   int err_gpu;
@@ -479,10 +479,12 @@ k_place(PlanParams P) {
       P.gpu_count[s] = 0;
       if (P.stats) {
         const long long z = (P.flags & IGP_F_STATS) ? 0 : -1;
-        P.stats[4 * s] = z;
-        P.stats[4 * s + 1] = z;
-        P.stats[4 * s + 2] = z;
-        P.stats[4 * s + 3] = 0;
+        P.stats[IGP_NSTAT * s] = z;
+        P.stats[IGP_NSTAT * s + 1] = z;
+        P.stats[IGP_NSTAT * s + 2] = z;
+        P.stats[IGP_NSTAT * s + 3] = 0;
+        P.stats[IGP_NSTAT * s + 4] = z;
+        P.stats[IGP_NSTAT * s + 5] = 0;
       }
     }
     continue;
@@ -508,8 +510,8 @@ k_place(PlanParams P) {
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
   int G = P.stream ? sst[0] : 0;
-  long long tot_evals = 0, tot_calls = 0, tot_cands = 0;
-  long long st_evals = 0, st_calls = 0, st_cands = 0;
+  long long tot_evals = 0, tot_calls = 0, tot_cands = 0, tot_rres = 0, tot_run = 0;
+  long long st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
   int fail_code = 0;
   ErrOut eo_fail;
   eo_fail.code = 0;
@@ -682,6 +684,8 @@ k_place(PlanParams P) {
                 c_occ = (int)(g & 0xffffu);
                 c_nres = (int)((g >> 16) & 0xffffu);
                 c_off = (int)(g >> 32);
+                st_rres += c_nres;
+                st_run += 1;
                 {  // stage the resident tile: one bulk copy group per candidate
                   const int nst = c_nres < SLOT ? c_nres : SLOT;
                   const uint32_t brec = (uint32_t)nst * (R_NF * 8);
@@ -949,12 +953,14 @@ k_place(PlanParams P) {
     if (gs.err_flag) {
       // exact mode only: replay the step in the reference's candidate order to
       // find the first raising candidate and the PlanStats at that point
-      st_evals = st_calls = st_cands = 0;
+      st_evals = st_calls = st_cands = st_rres = st_run = 0;
       if (wi == 0) run_step(true);
-      if (t != 0) st_evals = st_calls = st_cands = 0;
+      if (t != 0) st_evals = st_calls = st_cands = st_rres = st_run = 0;
       tot_evals += st_evals;
       tot_calls += st_calls;
       tot_cands += st_cands;
+      tot_rres += st_rres;
+      tot_run += st_run;
       if (P.stream) {  // the arrival is rejected; the state is unchanged
         if (t == 0) {
           P.code[sm + k] = eo_fail.code | (aflags << 8);
@@ -962,7 +968,7 @@ k_place(PlanParams P) {
           P.pos[sm + k] = -1;
           P.units[sm + k] = 0;
         }
-        st_evals = st_calls = st_cands = 0;
+        st_evals = st_calls = st_cands = st_rres = st_run = 0;
         group_sync<GW>();
         continue;
       }
@@ -972,7 +978,9 @@ k_place(PlanParams P) {
     tot_evals += st_evals;
     tot_calls += st_calls;
     tot_cands += st_cands;
-    st_evals = st_calls = st_cands = 0;
+    tot_rres += st_rres;
+    tot_run += st_run;
+    st_evals = st_calls = st_cands = st_rres = st_run = 0;
     const unsigned long long bk = gs.best;
     if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
     group_sync<GW>();
@@ -1141,18 +1149,22 @@ k_place(PlanParams P) {
   }
 
   // group totals of the counters
-  if (t == 0) gs.tot[0] = gs.tot[1] = gs.tot[2] = 0;
+  if (t == 0) gs.tot[0] = gs.tot[1] = gs.tot[2] = gs.tot[3] = gs.tot[4] = 0;
   group_sync<GW>();
   atomicAdd(&gs.tot[0], (unsigned long long)tot_evals);
   atomicAdd(&gs.tot[1], (unsigned long long)tot_calls);
   atomicAdd(&gs.tot[2], (unsigned long long)tot_cands);
+  atomicAdd(&gs.tot[3], (unsigned long long)tot_rres);
+  atomicAdd(&gs.tot[4], (unsigned long long)tot_run);
   group_sync<GW>();
   if (t == 0 && P.stats) {
     const bool st_ok = (P.flags & IGP_F_STATS) || fail_code == 1;
-    P.stats[4 * s] = st_ok ? (long long)gs.tot[0] : -1;
-    P.stats[4 * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
-    P.stats[4 * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
-    P.stats[4 * s + 3] = (long long)gs.tot[1];
+    P.stats[IGP_NSTAT * s] = st_ok ? (long long)gs.tot[0] : -1;
+    P.stats[IGP_NSTAT * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
+    P.stats[IGP_NSTAT * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
+    P.stats[IGP_NSTAT * s + 3] = (long long)gs.tot[1];
+    P.stats[IGP_NSTAT * s + 4] = st_ok ? (long long)gs.tot[3] : -1;
+    P.stats[IGP_NSTAT * s + 5] = (long long)gs.tot[4];
   }
 
   if (P.stream && t == 0) {  // persist the scenario state for the next push

@@ -45,7 +45,7 @@ class StreamPlanner:
                                                          self.b_max, self.flags))
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._out = torch.empty((3, self.S, self.C), dtype=torch.int32, device=self.device)
-        self.stats = torch.zeros((self.S, 4), dtype=torch.int64, device=self.device)
+        self.stats = torch.zeros((self.S, 6), dtype=torch.int64, device=self.device)
         self.reset()
 
     def _stream(self):

@@ -121,6 +121,7 @@ def _compare_to_oracle(res, s, wl, hw_vec, b_max, rank, oracle, stats=False):
     if stats:
         assert int(res["stats"][s][0]) == o["model_evals"]
         assert int(res["stats"][s][1]) == o["candidate_gpus"]
+        assert int(res["stats"][s][4]) == o["resident_reads"]
     return o
 
 

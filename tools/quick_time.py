@@ -22,7 +22,7 @@ for S, m, flags in cfgs:
     d_rk = torch.from_numpy(name_ranks(list(names))).to(dev)
     i32 = torch.empty((5, S, m), dtype=torch.int32, device=dev)
     d_gc = torch.empty(S, dtype=torch.int32, device=dev)
-    d_st = torch.empty((S, 4), dtype=torch.int64, device=dev)
+    d_st = torch.empty((S, 6), dtype=torch.int64, device=dev)
     d_err = torch.empty((S, 40), dtype=torch.uint8, device=dev)
     ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, 32, flags), dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
