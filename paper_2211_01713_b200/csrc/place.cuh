@@ -552,11 +552,6 @@ k_place(PlanParams P) {
       gs.err_flag = 0;
     }
     for (int x = t; x < TB * 4; x += GT) ntab[x] = tbl[(size_t)k * TB * 4 + x];
-    if (t == 0 && k + 1 < P.k1) {  // the next newcomer's rows
-      prefetch_l2(cold + (size_t)(k + 1) * C_NF, C_NF * 8);
-      prefetch_l2(nwt + (size_t)(k + 1) * R_NF, R_NF * 8);
-      prefetch_l2(tbl + (size_t)(k + 1) * TB * 4, TB * 32);
-    }
     group_sync<GW>();
     unsigned long long my_best = NO_KEY;
 
@@ -581,14 +576,6 @@ k_place(PlanParams P) {
       double c_C = 0.0, c_scale = 1.0, c_inv = 1.0, c_tsn = 0.0;
       double c_nka = 0.0, c_npw = 0.0, c_nca = 0.0;
       bool stop = false;
-
-      auto prefetch_tile = [&](unsigned long long g, int j) {
-        const int nr = (int)((g >> 16) & 0xffffu), of = (int)(g >> 32);
-        const int nst = nr < SLOT ? nr : SLOT;
-        prefetch_l2(rec + (size_t)of * R_NF, (uint32_t)nst * (R_NF * 8));
-        prefetch_l2(meta + of, (uint32_t)((nst + 1) >> 1) * 16u);
-        prefetch_l2(gfold + (size_t)j * 4, 32u);
-      };
 
       auto finish = [&](int result) {
         if (result == R_ERROR) {
@@ -654,18 +641,14 @@ k_place(PlanParams P) {
               if (lane >= o) incl += v;
             }
             int qp = qtail + incl - cnt;
-            // queued candidates are taken some iterations later: start pulling
-            // their tiles into L2 now so the lane's tile copy is an L2 hit
             if (bits & 1u) {
               q[qp & (QN - 1)] = jb;
               qg[qp & (QN - 1)] = g2.x;
               ++qp;
-              prefetch_tile(g2.x, jb);
             }
             if (bits & 2u) {
               q[qp & (QN - 1)] = jb + 1;
               qg[qp & (QN - 1)] = g2.y;
-              prefetch_tile(g2.y, jb + 1);
             }
             qtail += __shfl_sync(FULL, incl, 31);
             scan += scan_stride;
@@ -738,9 +721,7 @@ k_place(PlanParams P) {
         if (cj < 0) continue;
         if (c_need) {
           if (c_wait) {
-            // the tile is not here yet: this lane sits the iteration out and
-            // the warp's other lanes go on (a blocking wait would stall them)
-            if (!mbar_test(&sl->mbar, c_phase)) continue;
+            mbar_wait(&sl->mbar, c_phase);
             c_phase ^= 1u;
             c_wait = false;
           }
