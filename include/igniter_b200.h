@@ -101,8 +101,12 @@ enum {
   IGP_F_STATS = 1,      /* exact PlanStats (model_evals, candidate_gpus) for every
                            scenario: no overflow early exit, no bound prune */
   IGP_F_NO_PRED = 2,    /* skip the _build_plan breakdown rows */
-  IGP_F_CTA = 4         /* one CTA (many warps) per scenario instead of one warp:
+  IGP_F_CTA = 4,        /* one CTA (many warps) per scenario instead of one warp:
                            lower latency for single large plans */
+  IGP_F_COOP = 16       /* single scenario (n_scen == 1): every warp of the GPU
+                           shares each step (grid-cooperative launch); falls back
+                           on the device to IGP_F_CTA when the exact sequence is
+                           needed (IGP_F_STATS, or a scenario that can raise) */
 };
 
 int igp_abi_version(void);

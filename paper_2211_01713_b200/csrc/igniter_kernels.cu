@@ -385,6 +385,34 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
   }
 }
 
+// One scenario on the whole GPU: the cooperative step kernel, then the
+// per-CTA kernel, which writes the plan (or, when the cooperative kernel
+// declined because the exact sequence is needed, plans it itself).
+template <int MAXN>
+static int launch_place_coop(PlanParams P, cudaStream_t st) {
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_place<MAXN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)place_smem<1>());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place<MAXN, 1, true>, 128,
+                                                      place_smem<1>()) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+  }
+  int grid = per_sm * sms;
+  if (grid * 128 > COOP_MAX_LANES) grid = COOP_MAX_LANES / 128;
+  CK(cudaMemsetAsync(P.coop, 0, sizeof(CoopState), st));
+  CK(cudaMemsetAsync(P.coop->best, 0xff, sizeof(P.coop->best), st));
+  void *args[] = {&P};
+  CK(cudaLaunchCooperativeKernel((const void *)k_place<MAXN, 1, true>, dim3(grid), dim3(128), args,
+                                 place_smem<1>(), st));
+  launch_place<MAXN>(P, st);
+  return IGP_E_OK;
+}
+
 extern "C" {
 
 int igp_abi_version(void) { return IGP_ABI_VERSION; }
@@ -421,6 +449,8 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.stream = 0;
   P.code = nullptr;
   P.sstate = nullptr;
+  P.coop = (flags & IGP_F_COOP) && n_scen == 1 ? (CoopState *)(ws + L.coop) : nullptr;
+  P.win_tid = (int32_t *)(ws + L.win_tid);
   P.wl = wl;
   P.rank = name_rank;
   P.rank_stride = rank_stride;
@@ -464,9 +494,19 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
     }
   }
   if (stages & 2) {
-    if (hw.cap <= 48) launch_place<48>(P, st);
-    else if (hw.cap <= 128) launch_place<128>(P, st);
-    else launch_place<256>(P, st);
+    if (P.coop) {
+      int rc;
+      if (hw.cap <= 48) rc = launch_place_coop<48>(P, st);
+      else if (hw.cap <= 128) rc = launch_place_coop<128>(P, st);
+      else rc = launch_place_coop<256>(P, st);
+      if (rc) return rc;
+    } else if (hw.cap <= 48) {
+      launch_place<48>(P, st);
+    } else if (hw.cap <= 128) {
+      launch_place<128>(P, st);
+    } else {
+      launch_place<256>(P, st);
+    }
   }
   CK(cudaGetLastError());
   return IGP_E_OK;
@@ -667,6 +707,8 @@ static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const 
   P.units = (int32_t *)(ws + X.units);
   P.pred = nullptr;
   P.sstate = (int32_t *)(ws + X.sstate);
+  P.coop = nullptr;
+  P.win_tid = (int32_t *)(ws + L.win_tid);
   P.gpu_count = (int32_t *)(ws + X.gc);
   P.stats = nullptr;
   P.err = (igp_error *)(ws + X.err);

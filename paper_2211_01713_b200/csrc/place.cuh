@@ -112,9 +112,23 @@ __device__ __forceinline__ void fence_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Grid-cooperative single plan (IGP_F_COOP): every warp of the GPU works on
+// one scenario's step; the last warp to finish the step commits it and
+// publishes the step number.  State shared by all warps:
+struct CoopState {
+  unsigned long long best[2];  // argmin key of step k in best[k & 1]
+  int done[2];                 // warps finished with step k
+  int flag;                    // steps committed so far
+  int pool_top, abort, G;
+  int status;                  // 0 running, m completed, -1 declined (exact path needed)
+  int pad;
+  unsigned long long evals_run, cands_run;
+};
+constexpr int COOP_MAX_LANES = 160 * 512;  // lane_units rows reserved for the cooperative grid
+
 struct WsLayout {
   size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
-      lane_units, sflags, perr, sched, total;
+      lane_units, sflags, perr, sched, coop, win_tid, total;
   int lanes;
   int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
@@ -133,7 +147,7 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const size_t mm = (size_t)(m > 0 ? m : 1);
   const size_t Sm = (size_t)S * mm;
   const int capx = cap > 0 ? cap : 1;
-  L.lanes = (flags & IGP_F_CTA) ? 256 : 32;
+  L.lanes = (flags & IGP_F_COOP) ? COOP_MAX_LANES : (flags & IGP_F_CTA) ? 256 : 32;
   L.pool_recs = (long long)pool_factor(flags) * (long long)mm + 4 * TILE0;
   const size_t Sp = (size_t)S * (size_t)L.pool_recs;
   L.by_rank = off; off = align_up(off + Sm * 4);
@@ -153,6 +167,8 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.sflags = off; off = align_up(off + (size_t)S * 4);
   L.perr = off; off = align_up(off + (size_t)S * 4);
   L.sched = off; off = align_up(off + 4);
+  L.coop = off; off = align_up(off + sizeof(CoopState));
+  L.win_tid = off; off = align_up(off + ((flags & IGP_F_COOP) ? mm * 4 : 4));
   L.total = off;
   return L;
 }
@@ -168,6 +184,8 @@ struct PlanParams {
   int k0, k1, stream;
   int32_t *code;    // stream: per arrival error code | risk flags << 8
   int32_t *sstate;  // stream: per scenario {G, pool_top, sticky flags, arrivals}
+  CoopState *coop;  // cooperative single plan: shared step state (nullable)
+  int32_t *win_tid; // cooperative: thread whose lane_units hold candidate j's units
   const double *wl;     // [S][16][m]
   const int32_t *rank;  // name ranks
   int rank_stride;
@@ -428,9 +446,15 @@ struct LaneArrays {  // values of residents bumped inside the current candidate
 
 // One scenario per group of GW warps (GW == 1: four scenarios per 128-thread
 // CTA; GW > 1: one scenario per CTA).
-template <int MAXN, int GW>
+__device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p) {
+  return __ldcg(p);
+}
+__device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
+
+template <int MAXN, int GW, bool COOP = false>
 __global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32, GW == 1 ? IGP_MINB_WARP : 1)
 k_place(PlanParams P) {
+  static_assert(!COOP || GW == 1, "cooperative mode runs one group per warp");
   constexpr int GT = GW * 32;
   constexpr int GPB = (GW == 1) ? 4 : 1;
   constexpr unsigned long long NO_KEY = ~0ull;
@@ -447,14 +471,23 @@ k_place(PlanParams P) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   uint32_t c_phase = 0;  // parity of this lane's mbarrier
+  CoopState *const cs = P.coop;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;      // cooperative lane id
+  const int gwarp = gtid >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   // Persistent groups: each pulls the next scenario when it finishes one, so
   // scenarios of unequal length do not leave SMs idle at the end.
-  for (;;) {
-  if (t == 0) gs.next = atomicAdd(P.sched, 1);
-  group_sync<GW>();
-  const int s = gs.next;
-  group_sync<GW>();
-  if (s >= P.S) break;
+  for (int pass = 0;; ++pass) {
+  int s;
+  if constexpr (COOP) {
+    if (pass) break;
+    s = 0;
+  } else {
+    if (t == 0) gs.next = atomicAdd(P.sched, 1);
+    group_sync<GW>();
+    s = gs.next;
+    group_sync<GW>();
+    if (s >= P.S) break;
+  }
   int *q = qsm[grp * GW + wi];
   unsigned long long *qg = qgs[grp * GW + wi];
   double *ntab = ntb[grp];
@@ -505,24 +538,42 @@ k_place(PlanParams P) {
   int32_t *sst = P.stream ? P.sstate + 4 * (size_t)s : nullptr;
   // stream mode: risk flags of admitted arrivals stick to the scenario
   int sflags = P.stream ? sst[2] : P.sflags[s];
+  if constexpr (COOP) {
+    // the exact evaluation sequence (PlanStats, a scenario that can raise)
+    // runs in the per-CTA kernel; so does a scenario with a prologue error
+    if (P.perr[0] != INT_MAX || (sflags & SF_RISKY) || (P.flags & IGP_F_STATS)) {
+      if (gtid == 0) cs->status = -1;
+      return;
+    }
+  }
+  // a cooperative plan that already ran its steps: only the predictions remain
+  const bool coop_done = !COOP && P.coop && ld_cg(&P.coop->status) == P.m;
   const unsigned lt = (1u << lane) - 1u;
 
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
-  int G = P.stream ? sst[0] : 0;
+  int G = P.stream ? sst[0] : (coop_done ? P.coop->G : 0);
   long long tot_evals = 0, tot_calls = 0, tot_cands = 0, tot_rres = 0, tot_run = 0;
   long long st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
   int fail_code = 0;
   ErrOut eo_fail;
   eo_fail.code = 0;
   eo_fail.k = -1;
-  if (t == 0) {
-    gs.pool_top = P.stream ? sst[1] : 0;
+  int *poolp = &gs.pool_top, *abortp = &gs.abort_code;
+  if constexpr (COOP) {
+    poolp = &cs->pool_top;
+    abortp = &cs->abort;
+  } else if (t == 0) {
+    gs.pool_top = P.stream ? sst[1] : (coop_done ? P.coop->pool_top : 0);
     gs.abort_code = 0;
   }
   group_sync<GW>();
+  if (coop_done && t == 0) {
+    tot_run = (long long)P.coop->cands_run;
+    tot_calls = (long long)P.coop->evals_run;
+  }
 
-  for (int k = P.k0; k < P.k1; ++k) {
+  for (int k = coop_done ? P.k1 : P.k0; k < P.k1; ++k) {
     int aflags = 0;  // this arrival's risk flags (stream mode)
     if (P.stream) {
       const int c = P.code[sm + k];
@@ -566,8 +617,8 @@ k_place(PlanParams P) {
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
     auto run_step = [&](const bool serial) {
       int qhead = 0, qtail = 0;
-      int scan = serial ? 0 : wi * 64;
-      const int scan_stride = serial ? 64 : GT * 2;
+      int scan = serial ? 0 : (COOP ? gwarp * 64 : wi * 64);
+      const int scan_stride = serial ? 64 : (COOP ? nwarps * 64 : GT * 2);
       const unsigned take_mask = serial ? 1u : FULL;
       int cj = -1, c_nres = 0, c_occ = 0, c_sum = 0, c_i = 0, c_dirty = 0, c_off = 0;
       int c_pend = -1, c_pcode = 0, c_nu = 0;
@@ -603,13 +654,15 @@ k_place(PlanParams P) {
               ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
           if (key < my_best) {
             my_best = key;
-            uint16_t *lu = lane_units + (size_t)t * cap;
+            if constexpr (COOP) P.win_tid[cj] = gtid;
+            uint16_t *lu = lane_units + (size_t)(COOP ? gtid : t) * cap;
             for (int qq = 0; qq < c_nres; ++qq)
               lu[qq] = qq < SLOT ? sl->meta[qq].u
                                  : (mod.test(qq) ? (uint16_t)L.u[qq] : meta[c_off + qq].u);
             lu[c_nres] = (uint16_t)c_nu;
           }
           atomicMin(&gs.best, key);
+          if constexpr (COOP) atomicMin(&cs->best[k & 1], key);
         }
         cj = -1;
       };
@@ -620,6 +673,10 @@ k_place(PlanParams P) {
         const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
         if (idle) {
           const int nidle = __popc(idle);
+          if constexpr (COOP) {  // the other warps' results prune this warp's candidates
+            if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[k & 1]));
+            __syncwarp();
+          }
           // prefilter occupied + need <= cap (planner.py:297-299): two GPU
           // descriptors per lane per 16-byte load; passing (j, descriptor)
           // pairs are appended in ascending j
@@ -962,19 +1019,38 @@ k_place(PlanParams P) {
     tot_rres += st_rres;
     tot_run += st_run;
     st_evals = st_calls = st_cands = st_rres = st_run = 0;
-    const unsigned long long bk = gs.best;
-    if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
-    group_sync<GW>();
+    unsigned long long bk;
+    bool committer;
+    if constexpr (COOP) {
+      // arrive; the last warp to finish the step commits it, the others
+      // wait until it is published
+      __threadfence();  // this warp's keys, units and win_tid before its arrival
+      int last = 0;
+      if (lane == 0) last = atomicAdd(&cs->done[k & 1], 1) == nwarps - 1;
+      committer = __shfl_sync(FULL, last, 0) != 0;
+      if (!committer) {
+        if (lane == 0)
+          while (ld_cg(&cs->flag) <= k) __nanosleep(32);
+        __syncwarp();
+      }
+      __threadfence();  // acquire: later loads must not hit this SM's stale L1 lines
+      bk = ld_cg(&cs->best[k & 1]);
+    } else {
+      bk = gs.best;
+      if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
+      group_sync<GW>();
+      committer = wi == 0;
+    }
 
-    // ---- commit (planner.py:312-319), warp 0 of the group ----
-    if (wi == 0) {
+    // ---- commit (planner.py:312-319), one warp of the group ----
+    if (committer) {
       if (bk == NO_KEY) {
         if (lane == 0) {
-          const int off = gs.pool_top;
+          const int off = *poolp;
           if (off + TILE0 > P.pool_recs) {
-            gs.abort_code = IGP_E_CAPACITY;
+            *abortp = IGP_E_CAPACITY;
           } else {
-            gs.pool_top = off + TILE0;
+            *poolp = off + TILE0;
             gcap[G] = TILE0;
             gstate[G] = ((unsigned long long)off << 32) | (unsigned)need | (1u << 16);
             double *r = rec + (size_t)off * R_NF;
@@ -1014,7 +1090,8 @@ k_place(PlanParams P) {
         }
       } else {
         const int j = (int)(bk & 0xffffffffu);
-        const uint16_t *lu = lane_units + (size_t)gs.win_thread * cap;
+        const int wt = COOP ? P.win_tid[j] : gs.win_thread;
+        const uint16_t *lu = lane_units + (size_t)wt * cap;
         const int nres = (int)((gstate[j] >> 16) & 0xffffu);
         const int n = nres + 1;
         int off = (int)(gstate[j] >> 32);
@@ -1022,13 +1099,13 @@ k_place(PlanParams P) {
         if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
           int noff = 0;
           if (lane == 0) {
-            noff = gs.pool_top;
-            if (noff + 2 * tcap > P.pool_recs) gs.abort_code = IGP_E_CAPACITY;
-            else gs.pool_top = noff + 2 * tcap;
+            noff = *poolp;
+            if (noff + 2 * tcap > P.pool_recs) *abortp = IGP_E_CAPACITY;
+            else *poolp = noff + 2 * tcap;
           }
           noff = __shfl_sync(FULL, noff, 0);
           __syncwarp();
-          if (gs.abort_code == 0) {
+          if (*(volatile int *)abortp == 0) {
             for (int r = lane; r < nres; r += 32) {
 #pragma unroll
               for (int f = 0; f < R_NF; ++f)
@@ -1042,7 +1119,7 @@ k_place(PlanParams P) {
           }
           __syncwarp();
         }
-        if (gs.abort_code == 0) {
+        if (*(volatile int *)abortp == 0) {
           const double dnext = delta_sch(hw, n + 1);
           int part = 0;
           for (int r = lane; r < n; r += 32) {
@@ -1120,13 +1197,46 @@ k_place(PlanParams P) {
     }
     if (bk == NO_KEY) G += 1;
     sflags |= aflags;  // an admitted risky arrival can raise in later steps
-    if (wi == 0) fence_async_global();  // commit writes -> next step's tile copies
+    if (committer) fence_async_global();  // commit writes -> next step's tile copies
+    if constexpr (COOP) {
+      if (committer) {  // recycle step k-1's slots for step k+1, then publish step k
+        if (lane == 0) {
+          cs->done[(k + 1) & 1] = 0;
+          cs->best[(k + 1) & 1] = NO_KEY;
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(&cs->flag, k + 1);
+      }
+      if (ld_cg(abortp)) {
+        fail_code = 2;
+        break;
+      }
+      continue;
+    }
     __threadfence_block();
     group_sync<GW>();
     if (gs.abort_code) {
       fail_code = 2;
       break;
     }
+  }
+  if constexpr (COOP) {  // hand the state to the kernel that writes the plan
+    unsigned long long ev = (unsigned long long)tot_calls, cd = (unsigned long long)tot_run;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ev += __shfl_xor_sync(FULL, ev, o);
+      cd += __shfl_xor_sync(FULL, cd, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&cs->evals_run, ev);
+      atomicAdd(&cs->cands_run, cd);
+    }
+    if (gtid == 0 && !fail_code) {
+      cs->G = G;
+      cs->status = P.m;
+    }
+    return;
   }
 
   // group totals of the counters

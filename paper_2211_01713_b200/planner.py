@@ -44,6 +44,8 @@ from .model import (
 DEFAULT_BATCH_CAP = 32
 IGP_F_STATS = 1
 IGP_F_CTA = 4
+IGP_F_COOP = 16
+COOP_MIN_WORKLOADS = 256  # below this one warp per plan has lower latency
 
 
 @dataclass
@@ -265,6 +267,10 @@ def plan(
     flags = IGP_F_STATS if stats is not None else 0
     if m >= 4096:
         flags |= IGP_F_CTA  # one CTA per plan: many warps share each step's candidates
+    if m >= COOP_MIN_WORKLOADS:
+        # every warp of the GPU shares each step; the device falls back to the
+        # per-CTA kernel when the exact sequence is needed (stats, raising input)
+        flags |= IGP_F_COOP | IGP_F_CTA
     res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags)
     rec = res["err"][0]
     if stats is not None:

@@ -27,10 +27,11 @@ def test_c3_100k_plan_bit_exact():
     import make_c3_100k as C3
     from paper_2211_01713_b200 import _device
     from paper_2211_01713_b200.layout import hw_vector
-    from paper_2211_01713_b200.planner import IGP_F_CTA, name_ranks
+    from paper_2211_01713_b200.planner import IGP_F_COOP, IGP_F_CTA, name_ranks
     d = G.load("c3_plan_100k")
     hw, wl, names = C3.instance()
-    res = _device.plan_device(wl, hw_vector(hw), C3.B_MAX, name_ranks(names), flags=IGP_F_CTA)
+    res = _device.plan_device(wl, hw_vector(hw), C3.B_MAX, name_ranks(names),
+                              flags=IGP_F_CTA | IGP_F_COOP)
     assert int(res["err"][0]["code"]) == 0
     assert int(res["gpu_count"][0]) == int(d["gpu_count"])
     for k in ("gpu_of", "pos", "units", "batch", "lb"):

@@ -14,7 +14,8 @@ from instances import (c3_instance, hw_from_golden, make_v100, random_instance,
 import paper_2211_01713_b200 as igp
 from paper_2211_01713_b200 import _device, errors
 from paper_2211_01713_b200.layout import hw_vector
-from paper_2211_01713_b200.planner import IGP_F_CTA, IGP_F_STATS, name_ranks, workload_table
+from paper_2211_01713_b200.planner import (IGP_F_COOP, IGP_F_CTA, IGP_F_STATS, name_ranks,
+                                           workload_table)
 
 pytestmark = pytest.mark.gpu
 
@@ -250,3 +251,38 @@ def test_twelve_workload_order_invariance():
     b = igp.plan(list(reversed(w)), hw)
     assert [[(x.workload, x.r, x.batch) for x in g.allocations] for g in a.gpus] == \
            [[(x.workload, x.r, x.batch) for x in g.allocations] for g in b.gpus]
+
+
+@pytest.mark.parametrize("case", G.names("plan_"))
+@pytest.mark.parametrize("flags", [IGP_F_COOP, IGP_F_COOP | IGP_F_CTA, IGP_F_COOP | IGP_F_STATS])
+def test_cooperative_single_plan_matches_reference_golden(case, flags):
+    """Grid-cooperative single plan (and its device-side fallback for stats /
+    raising inputs) against the reference fixtures."""
+    d = G.load(case)
+    rank = name_ranks([str(n) for n in d["names"]])
+    res = _device.plan_device(d["wl"], d["hw"], int(d["b_max"]), rank, flags=flags)
+    if str(d["err_class"]):
+        assert int(res["err"][0]["code"]) == int(d["err_code"])
+        return
+    assert int(res["err"][0]["code"]) == 0
+    for k in ("gpu_of", "pos", "units", "batch", "lb"):
+        np.testing.assert_array_equal(res[k][0], d[k], err_msg=k)
+    np.testing.assert_array_equal(G.bits(res["pred"][0]), G.bits(d["pred"]))
+    if flags & IGP_F_STATS:
+        assert int(res["stats"][0][0]) == int(d["model_evals"])
+        assert int(res["stats"][0][1]) == int(d["candidate_gpus"])
+
+
+def test_cooperative_10k_and_r01_vs_oracle(oracle_lib):
+    from paper_2211_01713_b200 import synth
+    hw = make_v100()
+    wl, names = synth.scenarios(1, 10_000, hw, seed=91)
+    rank = name_ranks(list(names))
+    res = _device.plan_device(wl, hw_vector(hw), 32, rank, flags=IGP_F_COOP | IGP_F_CTA)
+    _compare_to_oracle(res, 0, wl[0], np.array(hw_vector(hw)), 32, rank, oracle_lib)
+    hw = make_v100(r_unit=0.01)
+    wl, names = synth.scenarios(1, 3000, hw, seed=92, slo=(20.0, 100.0), rate=(50.0, 6000.0),
+                                b_max=128)
+    rank = name_ranks(list(names))
+    res = _device.plan_device(wl, hw_vector(hw), 128, rank, flags=IGP_F_COOP)
+    _compare_to_oracle(res, 0, wl[0], np.array(hw_vector(hw)), 128, rank, oracle_lib)

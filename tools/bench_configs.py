@@ -29,7 +29,7 @@ import torch  # noqa: E402
 
 from paper_2211_01713_b200 import _device, _native, synth  # noqa: E402
 from paper_2211_01713_b200.layout import hw_vector  # noqa: E402
-from paper_2211_01713_b200.planner import IGP_F_CTA, IGP_F_STATS, name_ranks  # noqa: E402
+from paper_2211_01713_b200.planner import IGP_F_COOP, IGP_F_CTA, IGP_F_STATS, name_ranks  # noqa: E402
 
 dev = torch.device("cuda", 0)
 lib = _native.lib_for_compute()
@@ -124,12 +124,13 @@ def c2():
     wl, names = synth.scenarios(1, 1000, hw, seed=7)
     rk = name_ranks(list(names))
     out = {}
-    for tag, fl in (("warp", 0), ("cta", IGP_F_CTA)):
+    for tag, fl in (("warp", 0), ("cta", IGP_F_CTA), ("coop", IGP_F_COOP | IGP_F_CTA)):
         dp = DevicePlan(wl, hv, 32, rk, fl)
         out[tag] = dp.time(10)
     st = dp.ref_stats()
     emit(dict(config="C2", workload="1 plan of 1,000 synthetic workloads, r_unit 0.025, b<=32",
               ms_per_plan_warp=out["warp"], ms_per_plan_cta=out["cta"],
+              ms_per_plan_coop=out["coop"],
               us_per_step=min(out.values()) * 1e3 / 1000, reference_counters=st,
               candidate_evals_per_s=st["model_evals"] / (min(out.values()) / 1e3)))
 
@@ -142,10 +143,11 @@ def c3():
     wl, names = synth.scenarios(1, m, hw, seed=2211, slo=(20.0, 100.0), rate=(50.0, 6000.0),
                                 b_max=128)
     rk = name_ranks(list(names))
-    dp = DevicePlan(wl, hv, 128, rk, IGP_F_CTA)
+    dp = DevicePlan(wl, hv, 128, rk, IGP_F_CTA | IGP_F_COOP)
     plan_ms = dp.time(1)
     st = dp.ref_stats()
-    emit(dict(config="C3-plan", workload="1 plan of 100,000 workloads, r_unit 0.01, b<=128 (CTA mode)",
+    emit(dict(config="C3-plan", workload="1 plan of 100,000 workloads, r_unit 0.01, b<=128 "
+                                         "(grid-cooperative)",
               ms_per_plan=plan_ms, us_per_step=plan_ms * 1e3 / m, gpus=int(dp.gc[0].item()),
               reference_counters=st, candidate_evals_per_s=st["model_evals"] / (plan_ms / 1e3),
               cpu_oracle_s_per_plan=162.0,
