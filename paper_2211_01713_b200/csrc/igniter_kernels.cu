@@ -388,6 +388,10 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
 // One scenario on the whole GPU: the cooperative step kernel, then the
 // per-CTA kernel, which writes the plan (or, when the cooperative kernel
 // declined because the exact sequence is needed, plans it itself).
+#ifndef COOP_M_PER_CTA
+#define COOP_M_PER_CTA 64
+#endif
+
 template <int MAXN>
 static int launch_place_coop(PlanParams P, cudaStream_t st) {
   static int per_sm = -1, sms = 0;
@@ -404,6 +408,12 @@ static int launch_place_coop(PlanParams P, cudaStream_t st) {
   }
   int grid = per_sm * sms;
   if (grid * 128 > COOP_MAX_LANES) grid = COOP_MAX_LANES / 128;
+  // no more CTAs than the step's candidates can use (a step of m workloads has
+  // about m / 40 candidates at 2.5% units); bits 16..27 of flags override
+  const int want_ctas = (P.flags >> 16) & 0xfff;
+  const int by_m = (P.m + COOP_M_PER_CTA - 1) / COOP_M_PER_CTA;
+  const int lim = want_ctas ? want_ctas : (by_m > 1 ? by_m : 1);
+  if (grid > lim) grid = lim;
   CK(cudaMemsetAsync(P.coop, 0, sizeof(CoopState), st));
   CK(cudaMemsetAsync(P.coop->best, 0xff, sizeof(P.coop->best), st));
   void *args[] = {&P};

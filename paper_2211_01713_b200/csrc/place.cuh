@@ -624,7 +624,8 @@ k_place(PlanParams P) {
       int c_pend = -1, c_pcode = 0, c_nu = 0;
       unsigned c_sb = 0;  // staged residents already bumped inside this candidate
       bool c_flag = false, c_need = false, c_wait = false;
-      double c_C = 0.0, c_scale = 1.0, c_inv = 1.0, c_tsn = 0.0;
+      double c_C = 0.0, c_f = 0.0, c_inv = 1.0, c_tsn = 0.0;
+      bool c_one = true;  // f == F: scale = F / F = 1.0 and x / 1.0 == x
       double c_nka = 0.0, c_npw = 0.0, c_nca = 0.0;
       bool stop = false;
 
@@ -830,8 +831,13 @@ k_place(PlanParams P) {
           fc.add(c_nca);
           const double f = frequency(hw, hw.pidle + fp.result());
           c_C = fc.result();
-          c_scale = f / hw.fmax;
-          c_inv = (c_scale == 1.0) ? 1.0 : 1.0 / c_scale;
+          // t_gpu = x / scale with scale = f / F (model.py:305-310).  The
+          // decision t_inf > t_half uses x * (F / f), within 3 ulps of the
+          // quotient, and falls back to the literal x / (f / F) inside the
+          // margin; one division per evaluation instead of two.
+          c_f = f;
+          c_one = f == hw.fmax && hw.margin_ok;
+          c_inv = c_one ? 1.0 : hw.fmax / f;
           st_evals += c_nres + 1;
           st_calls += 1;
           c_need = false;
@@ -880,13 +886,13 @@ k_place(PlanParams P) {
           }
           const double x = t_sch + ka * (1.0 + acache * (c_C - ca));
           double t_gpu = x;  // x / 1.0 == x exactly
-          if (c_scale != 1.0) {
+          if (!c_one) {
             t_gpu = x * c_inv;
             if (margin) {
               const double tq = (t_load + t_gpu) + t_fb;
-              if (!(fabs(tq - t_half) > tq * 0x1p-48 + 0x1p-1000)) t_gpu = x / c_scale;
+              if (!(fabs(tq - t_half) > tq * 0x1p-48 + 0x1p-1000)) t_gpu = x / (c_f / hw.fmax);
             } else {
-              t_gpu = x / c_scale;
+              t_gpu = x / (c_f / hw.fmax);
             }
           }
           const double t_inf = (t_load + t_gpu) + t_fb;
@@ -1022,16 +1028,18 @@ k_place(PlanParams P) {
     unsigned long long bk;
     bool committer;
     if constexpr (COOP) {
-      // arrive; the last warp to finish the step commits it, the others
-      // wait until it is published
+      // arrive per CTA; warp 0 of the last CTA to finish the step commits
+      // it, the other CTAs wait until it is published
       __threadfence();  // this warp's keys, units and win_tid before its arrival
-      int last = 0;
-      if (lane == 0) last = atomicAdd(&cs->done[k & 1], 1) == nwarps - 1;
-      committer = __shfl_sync(FULL, last, 0) != 0;
-      if (!committer) {
-        if (lane == 0)
+      __syncthreads();
+      if (threadIdx.x == 0) gsm[0].next = atomicAdd(&cs->done[k & 1], 1) == (int)gridDim.x - 1;
+      __syncthreads();
+      const bool last_cta = gsm[0].next != 0;
+      committer = last_cta && wi == 0 && grp == 0;
+      if (!last_cta) {
+        if (threadIdx.x == 0)
           while (ld_cg(&cs->flag) <= k) __nanosleep(32);
-        __syncwarp();
+        __syncthreads();
       }
       __threadfence();  // acquire: later loads must not hit this SM's stale L1 lines
       bk = ld_cg(&cs->best[k & 1]);
@@ -1212,6 +1220,7 @@ k_place(PlanParams P) {
         fail_code = 2;
         break;
       }
+      __syncthreads();  // the CTA's committer may still use gsm[0].next
       continue;
     }
     __threadfence_block();
