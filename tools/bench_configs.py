@@ -180,6 +180,17 @@ def c3():
               note="scan stops at the first feasible u per (w, b) like best_group_alloc"))
 
 
+def c3grid():
+    """Only the solo grid of C3 (for a focused ncu capture)."""
+    from instances import make_v100
+    hw = make_v100(r_unit=0.01)
+    hv = np.array(hw_vector(hw))
+    m = 100_000
+    wl, _ = synth.scenarios(1, m, hw, seed=2211, slo=(20.0, 100.0), rate=(50.0, 6000.0), b_max=128)
+    r = _device.solo_grid(wl[0], hv, 128)
+    emit(dict(config="C3-grid-only", feasible_points=int((r["min_units"] > 0).sum())))
+
+
 def c4():
     from instances import make_v100
     hw = make_v100()
