@@ -103,6 +103,8 @@ enum {
   IGP_F_NO_PRED = 2,    /* skip the _build_plan breakdown rows */
   IGP_F_CTA = 4,        /* one CTA (many warps) per scenario instead of one warp:
                            lower latency for single large plans */
+  IGP_F_GW2 = 32,       /* two / four warps per scenario (between the default one */
+  IGP_F_GW4 = 64,       /* warp and IGP_F_CTA's eight) */
   IGP_F_COOP = 16       /* single scenario (n_scen == 1): every warp of the GPU
                            shares each step (grid-cooperative launch); falls back
                            on the device to IGP_F_CTA when the exact sequence is

@@ -31,6 +31,9 @@ namespace igp {
 #ifndef IGP_MINB_WARP
 #define IGP_MINB_WARP 4
 #endif
+#ifndef IGP_MINB_CTA
+#define IGP_MINB_CTA 1
+#endif
 
 static thread_local char g_last_err[256] = "";
 
@@ -380,6 +383,10 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
   cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
   if (P.flags & IGP_F_CTA) {
     k_place<MAXN, 8><<<place_grid<MAXN, 8>(P.S), 256, place_smem<8>(), st>>>(P);
+  } else if (P.flags & IGP_F_GW4) {
+    k_place<MAXN, 4><<<place_grid<MAXN, 4>(P.S), 128, place_smem<4>(), st>>>(P);
+  } else if (P.flags & IGP_F_GW2) {
+    k_place<MAXN, 2><<<place_grid<MAXN, 2>(P.S), 64, place_smem<2>(), st>>>(P);
   } else {
     k_place<MAXN, 1><<<place_grid<MAXN, 1>(P.S), 128, place_smem<1>(), st>>>(P);
   }

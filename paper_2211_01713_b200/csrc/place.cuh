@@ -147,7 +147,8 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const size_t mm = (size_t)(m > 0 ? m : 1);
   const size_t Sm = (size_t)S * mm;
   const int capx = cap > 0 ? cap : 1;
-  L.lanes = (flags & IGP_F_COOP) ? COOP_MAX_LANES : (flags & IGP_F_CTA) ? 256 : 32;
+  L.lanes = (flags & IGP_F_COOP) ? COOP_MAX_LANES : (flags & IGP_F_CTA) ? 256
+            : (flags & IGP_F_GW4) ? 128 : (flags & IGP_F_GW2) ? 64 : 32;
   L.pool_recs = (long long)pool_factor(flags) * (long long)mm + 4 * TILE0;
   const size_t Sp = (size_t)S * (size_t)L.pool_recs;
   L.by_rank = off; off = align_up(off + Sm * 4);
@@ -452,7 +453,8 @@ __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p)
 __device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
 
 template <int MAXN, int GW, bool COOP = false>
-__global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32, GW == 1 ? IGP_MINB_WARP : 1)
+__global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32,
+                                  GW == 1 ? IGP_MINB_WARP : GW == 2 ? 8 : GW == 4 ? 4 : IGP_MINB_CTA)
 k_place(PlanParams P) {
   static_assert(!COOP || GW == 1, "cooperative mode runs one group per warp");
   constexpr int GT = GW * 32;
