@@ -21,6 +21,9 @@
  *       the planner.py:290-319 step applied in arrival order to persistent
  *                                  device state (online re-provisioning; no
  *                                  reference API, see below)
+ *   igp_group_search_device
+ *       replaces _Search.best_group_alloc oracle.py:77-114 for every subset
+ *                                  of a small group (exhaustive_plan's search)
  *   igp_solo_grid_device
  *       replaces _Search.best_group_alloc oracle.py:77-114 for one-workload
  *                                  groups over every batch (the solo grid)
@@ -235,6 +238,23 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
                                double *pred, int32_t *gpu_count, igp_error *err,
                                void *workspace, size_t workspace_bytes, int flags,
                                void *stream);
+
+/*
+ * Exhaustive oracle group search (_Search.best_group_alloc, oracle.py:77-114)
+ * for every non-empty subset of n <= 6 workloads (in name order, the order
+ * of oracle.py:86) at once: best[mask] is the lexicographic minimum of
+ * (total units, unit tuple) over the feasible unit vectors drawn from grid
+ * (ascending, device) with total <= max_units, packed as
+ * total << 9k | u_1 << 9(k-1) | ... | u_k, or ~0 when none is feasible.
+ * Feasibility is _Search._feasible (oracle.py:64-75).  err (device int32)
+ * receives an IGP_E_DENOM / IGP_E_ACTIVE_TIME code if any enumerated vector
+ * raised (the reference raises only for the vectors its pruned recursion
+ * evaluates).  The reference's candidate budget (OracleBudget.max_candidates)
+ * counts its own pruned evaluations and is not reproduced.
+ */
+int igp_group_search_device(const double *wl, int n, const int32_t *batch, const double *hw,
+                            const int32_t *grid, int n_grid, unsigned long long *best,
+                            int32_t *err, void *stream);
 
 /*
  * Solo candidate grid (BASELINE config 3): every (workload w, batch b in

@@ -628,3 +628,59 @@ int igo_stream(const double *wl, int64_t ld, int n, const double *hw, int b_max,
   free(eps); free(cand); free(best); free(buf);
   return 0;
 }
+
+/* ---- exhaustive oracle group search: oracle.py:64-114 -----------------
+ * For every non-empty subset (members in the caller's order = name order,
+ * oracle.py:86) the lexicographic minimum of (total, unit tuple) over the
+ * feasible vectors on the grid with total <= max_units, packed like
+ * igp_group_search_device; ~0 when none.  Returns the first evaluation error
+ * code met (0 if none). */
+int igo_group_search(const double *wl, int64_t ld, int n, const int32_t *batch, const double *hw,
+                     const int32_t *grid, int n_grid, uint64_t *best) {
+  int cap = igo_max_units(hw);
+  int first_err = 0;
+  entry_t ents[8];
+  for (int w = 0; w < n; ++w) make_entry(&ents[w], wl, ld, w, batch[w], hw);
+  for (int mask = 1; mask < (1 << n); ++mask) {
+    int idx[8], k = 0;
+    for (int w = 0; w < n; ++w)
+      if ((mask >> w) & 1) idx[k++] = w;
+    uint64_t b = ~(uint64_t)0;
+    int digit[8] = {0};
+    for (;;) {
+      int sum = 0, units[8];
+      for (int d = 0; d < k; ++d) {
+        units[d] = grid[digit[d]];
+        sum += units[d];
+      }
+      if (sum <= cap) {
+        const entry_t *eps[8];
+        double rs[8], rows[80], scratch[24];
+        for (int d = 0; d < k; ++d) {
+          eps[d] = &ents[idx[d]];
+          rs[d] = (double)units[d] * hw[H_RUNIT];
+        }
+        igo_err e;
+        int rc = eval_entries(eps, rs, k, hw, rows, NULL, scratch, &e);
+        if (rc) {
+          if (!first_err) first_err = rc;
+        } else {
+          int ok = 1;
+          for (int d = 0; d < k && ok; ++d)
+            if (rows[10 * d + 6] > eps[d]->t_half || rows[10 * d + 7] < WLF(wl, ld, F_RATE, idx[d]))
+              ok = 0;
+          if (ok) {
+            uint64_t key = (uint64_t)sum;
+            for (int d = 0; d < k; ++d) key = (key << 9) | (uint64_t)units[d];
+            if (key < b) b = key;
+          }
+        }
+      }
+      int d = k - 1;
+      while (d >= 0 && ++digit[d] == n_grid) digit[d--] = 0;
+      if (d < 0) break;
+    }
+    best[mask] = b;
+  }
+  return first_err;
+}

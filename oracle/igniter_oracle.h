@@ -37,4 +37,6 @@ int igo_solo_grid(const double *wl, int64_t ld, int m, const double *hw, int b_m
 int igo_stream(const double *wl, int64_t ld, int n, const double *hw, int b_max,
                int32_t *gpu_of, int32_t *pos, int32_t *code, int32_t *units_final,
                int32_t *gpu_count, int64_t *stats);
+int igo_group_search(const double *wl, int64_t ld, int n, const int32_t *batch, const double *hw,
+                     const int32_t *grid, int n_grid, uint64_t *best);
 #endif

@@ -158,3 +158,17 @@ def stream(wl, hw, b_max: int):
                      _p(gpu_of), _p(pos), _p(code), _p(units), _p(gc), _p(st))
     return dict(gpu_of=gpu_of, pos=pos, code=code, units=units, gpu_count=int(gc[0]),
                 model_evals=int(st[0]), candidate_gpus=int(st[1]))
+
+
+def group_search(wl, batch, hw, grid):
+    """Per-subset minimal (total, units) keys of the exhaustive oracle
+    (oracle.py:77-114), packed like igp_group_search_device."""
+    wl = np.ascontiguousarray(wl, np.float64)
+    n = wl.shape[1]
+    hw = np.ascontiguousarray(hw, np.float64)
+    batch = np.ascontiguousarray(batch, np.int32)
+    grid = np.ascontiguousarray(grid, np.int32)
+    best = np.zeros(1 << n, np.uint64)
+    rc = lib().igo_group_search(_p(wl), ctypes.c_int64(n), ctypes.c_int(n), _p(batch), _p(hw),
+                                _p(grid), ctypes.c_int(len(grid)), _p(best))
+    return best, int(rc)

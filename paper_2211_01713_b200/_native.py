@@ -18,7 +18,7 @@ LIB_DIR = os.path.join(PKG, "_lib")
 LIB_PATH = os.environ.get("IGP_LIB") or os.path.join(LIB_DIR, "libigniter_b200.so")
 SOURCES = [os.path.join(PKG, "csrc", "igniter_kernels.cu")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", "exact_fp64.cuh"), os.path.join(PKG, "csrc", "place.cuh"),
-                  os.path.join(PKG, "csrc", "grid.cuh"),
+                  os.path.join(PKG, "csrc", "grid.cuh"), os.path.join(PKG, "csrc", "exhaustive.cuh"),
                   os.path.join(REPO, "include", "igniter_b200.h")]
 
 NVCC_FLAGS = [
@@ -92,6 +92,7 @@ PROTOTYPES = {
     "igp_alloc_units_device": (_I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _VP, _VP, _VP]),
     "igp_prologue_device": (_I, [_VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     "igp_solo_grid_device": (_I, [_VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP]),
+    "igp_group_search_device": (_I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _VP, _VP]),
     "igp_stream_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I]),
     "igp_stream_reset_device": (_I, [_I, _I, _VP, _I, _VP, _SZ, _I, _VP]),
     "igp_stream_push_device": (_I, [_VP, _I, _I, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _SZ,

@@ -133,6 +133,10 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 
 #include "place.cuh"
 #include "grid.cuh"
+#ifndef IGP_GS_MAXN
+#define IGP_GS_MAXN 6
+#endif
+#include "exhaustive.cuh"
 
 namespace igp {
 
@@ -832,6 +836,45 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
   }
   if (gpu_count) CK(cudaMemcpyAsync(gpu_count, ws + X.gc, S * 4, cudaMemcpyDeviceToDevice, st));
   if (err) CK(cudaMemcpyAsync(err, ws + X.err, S * sizeof(igp_error), cudaMemcpyDeviceToDevice, st));
+  return IGP_E_OK;
+}
+
+int igp_group_search_device(const double *wl, int n, const int32_t *batch, const double *hw_h,
+                            const int32_t *grid, int n_grid, unsigned long long *best,
+                            int32_t *err, void *stream) {
+  if (n < 1 || n > IGP_GS_MAXN || n_grid < 1 || !hw_h || !grid || !best || !err)
+    return IGP_E_ARG;
+  Hw hw = make_hw(hw_h, 0);
+  if (hw.cap < 1) return IGP_E_ARG;
+  if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  GroupSearchParams G;
+  G.hw = hw;
+  G.n = n;
+  G.n_grid = n_grid;
+  G.wl = wl;
+  G.batch = batch;
+  G.grid = grid;
+  G.best = best;
+  G.err = err;
+  long long acc = 0;
+  G.base[0] = 0;
+  for (int mask = 1; mask <= (1 << n); ++mask) {
+    G.base[mask] = acc;
+    if (mask == (1 << n)) break;
+    long long c = 1;
+    for (int b = 0; b < n; ++b)
+      if ((mask >> b) & 1) c *= n_grid;
+    acc += c;
+  }
+  G.base[1 << n] = acc;
+  CK(cudaMemsetAsync(best, 0xff, sizeof(unsigned long long) << n, st));
+  CK(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+  long long blocks = (acc + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks < 1) blocks = 1;
+  k_group_search<<<(unsigned)blocks, 256, 0, st>>>(G);
+  CK(cudaGetLastError());
   return IGP_E_OK;
 }
 

@@ -357,6 +357,33 @@ def stream_reference(workloads, hw, b_max=32):
     return gpu_of, pos, code, final_units
 
 
+def oracle_case(workloads, hw, budget=None, b_max=32):
+    """The reference's exhaustive_plan (oracle.py:130-201) on a tiny instance."""
+    from gpuplanner import oracle as goracle
+    out = pack_instance(workloads, hw, b_max)
+    grid = budget.r_grid_units if budget and budget.r_grid_units else ()
+    out.update(max_gpus=np.int64(budget.max_gpus if budget else 3), grid=np.array(grid, np.int64))
+    m = len(workloads)
+    try:
+        p = goracle.exhaustive_plan(workloads, hw, budget=budget, b_max=b_max)
+    except gerr.GpuPlannerError as exc:
+        out.update(err_class=np.array(type(exc).__name__), err_msg=np.array(str(exc)))
+        return out
+    idx = {s.name: i for i, (s, _) in enumerate(workloads)}
+    gpu_of = np.full(m, -1, np.int32)
+    units = np.zeros(m, np.int32)
+    pred = np.zeros((m, layout.ROW_NF))
+    for g in p.gpus:
+        for a in g.allocations:
+            i = idx[a.workload]
+            gpu_of[i] = g.gpu_index
+            units[i] = int(round(a.r / hw.r_unit))
+            pred[i] = [getattr(g.predicted[a.workload], f) for f in layout.ROW_FIELDS]
+    out.update(err_class=np.array(""), err_msg=np.array(""), gpu_of=gpu_of, units=units, pred=pred,
+               gpu_count=np.int64(len(p.gpus)), cost=np.float64(p.cost_per_hour))
+    return out
+
+
 def stream_case(workloads, hw, b_max=32):
     out = pack_instance(workloads, hw, b_max)
     gpu_of, pos, code, units = stream_reference(workloads, hw, b_max)
@@ -366,7 +393,7 @@ def stream_case(workloads, hw, b_max=32):
 
 
 def main():
-    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream"}
+    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream", "oracle"}
     mpath = os.path.join(HERE, "manifest.json")
     manifest = json.load(open(mpath))["cases"] if os.path.exists(mpath) else {}
     v100 = support.make_v100()
@@ -486,6 +513,31 @@ def main():
                + [denom_error_workload("s_negk", 0.05, k3=-3.0)] + inst[80:])
         save("stream_errors_124", stream_case(mix, v100),
              "stream with rejected arrivals: infeasible SLO, batch cap, r + k4 <= 0, k_act <= 0")
+
+    # ---- exhaustive oracle (oracle.py:130-201), SURVEY §8f row 2 -----------
+    if "oracle" in groups:
+        from gpuplanner import oracle as goracle
+        rng = np.random.default_rng(808)
+        for i in range(24):
+            m = 1 + i % 4
+            save(f"oracle_rand{i:02d}", oracle_case(support.random_instance(rng, m, v100), v100),
+                 f"exhaustive_plan on random_instance m={m}")
+        hw20 = support.make_v100(r_unit=0.05)
+        for i in range(4):
+            save(f"oracle_r05_{i}", oracle_case(support.random_instance(rng, 4, hw20), hw20),
+                 "exhaustive_plan, r_unit 0.05 (cap 20), 4 workloads")
+        coarse = goracle.OracleBudget(r_grid_units=(1, 2, 3, 5, 8, 13, 21, 34))
+        for i in range(3):
+            save(f"oracle_grid_{i}", oracle_case(support.random_instance(rng, 3, v100), v100, coarse),
+                 "exhaustive_plan with a custom unit grid")
+        heavy = [(gp.WorkloadSpec(f"h{i}", 30.0, 450.0, 0.9, 0.05), support.demo_coef(k3=6.0))
+                 for i in range(4)]
+        save("oracle_err_infeasible", oracle_case(heavy, v100, goracle.OracleBudget(max_gpus=1)),
+             "InfeasibleError: four heavy workloads on one device")
+        save("oracle_err_budget", oracle_case(support.random_instance(rng, 5, v100), v100),
+             "BudgetExceededError: five workloads")
+        save("oracle_twelve_sub4", oracle_case(support.twelve_workload_instance()[:4], v100),
+             "exhaustive_plan on the first four C1 workloads")
 
     # ---- component cases ------------------------------------------------
     if "component" not in groups:
