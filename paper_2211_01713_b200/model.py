@@ -151,8 +151,8 @@ class SloCheck:
 def slo_check(breakdown: LatencyBreakdown, spec: WorkloadSpec) -> SloCheck:
     """Half-SLO latency budget and arrival-rate floor (model.py:346-351)."""
     return SloCheck(
-        latency_ok=breakdown.t_inf_ms <= spec.slo_ms / 2.0,
-        throughput_ok=breakdown.throughput_rps >= spec.rate_rps,
+        latency_ok=bool(breakdown.t_inf_ms <= spec.slo_ms / 2.0),
+        throughput_ok=bool(breakdown.throughput_rps >= spec.rate_rps),
     )
 
 
@@ -233,4 +233,5 @@ def predict_gpu(
         return {}
     entries = [_Entry(specs[a.workload], coefs[a.workload], a.batch, hw) for a in allocations]
     rows = eval_states([(entries, [a.r for a in allocations])], hw, check_capacity=True)[0]
-    return {a.workload: LatencyBreakdown(*row) for a, row in zip(allocations, rows)}
+    return {a.workload: LatencyBreakdown(*(float(v) for v in row))
+            for a, row in zip(allocations, rows)}

@@ -181,7 +181,8 @@ def _build_plan(strategy, hw, placement, specs, coefs, lb_units) -> Plan:
     it = iter(rows_per_gpu)
     for index, ((names, units, batches), allocations) in enumerate(zip(placement, allocs_per_gpu)):
         rows = next(it) if allocations else []
-        predicted = {a.workload: LatencyBreakdown(*row) for a, row in zip(allocations, rows)}
+        predicted = {a.workload: LatencyBreakdown(*(float(v) for v in row))
+                     for a, row in zip(allocations, rows)}
         gpus.append(GpuPlan(index, allocations, predicted, (cap - sum(units)) * hw.r_unit))
         for nm, u in zip(names, units):
             r_inter[nm] = (u - lb_units[nm]) * hw.r_unit

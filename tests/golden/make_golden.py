@@ -393,7 +393,7 @@ def stream_case(workloads, hw, b_max=32):
 
 
 def main():
-    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream", "oracle"}
+    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream", "oracle", "document"}
     mpath = os.path.join(HERE, "manifest.json")
     manifest = json.load(open(mpath))["cases"] if os.path.exists(mpath) else {}
     v100 = support.make_v100()
@@ -538,6 +538,18 @@ def main():
              "BudgetExceededError: five workloads")
         save("oracle_twelve_sub4", oracle_case(support.twelve_workload_instance()[:4], v100),
              "exhaustive_plan on the first four C1 workloads")
+
+    # ---- plan documents (problem.py:305-341), SURVEY §8f row 1 -------------
+    if "document" in groups:
+        from gpuplanner import problem as gproblem
+        for name, wls, hw in (("doc_c1_twelve", support.twelve_workload_instance(), v100),
+                              ("doc_rand80", support.random_instance(np.random.default_rng(80), 80, v100), v100),
+                              ("doc_r01_40", support.random_instance(np.random.default_rng(81), 40, hw01), hw01)):
+            p = gp.plan(wls, hw)
+            doc = gproblem.plan_to_document(p, {s.name: s for s, _ in wls})
+            d = pack_instance(wls, hw, 32)
+            d.update(document=np.array(json.dumps(doc)))
+            save(name, d, "reference plan_to_document(plan(...)) as JSON text")
 
     # ---- component cases ------------------------------------------------
     if "component" not in groups:

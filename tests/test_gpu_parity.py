@@ -286,3 +286,21 @@ def test_cooperative_10k_and_r01_vs_oracle(oracle_lib):
     rank = name_ranks(list(names))
     res = _device.plan_device(wl, hw_vector(hw), 128, rank, flags=IGP_F_COOP)
     _compare_to_oracle(res, 0, wl[0], np.array(hw_vector(hw)), 128, rank, oracle_lib)
+
+
+@pytest.mark.parametrize("case", G.names("doc_"))
+def test_plan_document_matches_reference_text(case):
+    """plan_to_document (problem.py:305-341) of the device plan is the
+    reference's JSON document, character for character."""
+    import json
+    from paper_2211_01713_b200.document import allocations_from_document, plan_to_document
+    d = G.load(case)
+    wls = workloads_from_golden(d)
+    hw = hw_from_golden(d)
+    specs = {s.name: s for s, _ in wls}
+    doc = plan_to_document(igp.plan(wls, hw), specs)
+    assert json.dumps(doc) == str(d["document"])
+    rev = plan_to_document(igp.plan(list(reversed(wls)), hw), specs)  # test_planner.py:208-213
+    assert rev == doc
+    allocs = allocations_from_document(doc)
+    assert sum(len(a) for a in allocs) == len(wls)
