@@ -24,6 +24,8 @@
  *   igp_group_search_device
  *       replaces _Search.best_group_alloc oracle.py:77-114 for every subset
  *                                  of a small group (exhaustive_plan's search)
+ *   igp_simulate_device
+ *       replaces simulate() simulate.py:139-198 (constant-rate arrivals)
  *   igp_solo_grid_device
  *       replaces _Search.best_group_alloc oracle.py:77-114 for one-workload
  *                                  groups over every batch (the solo grid)
@@ -255,6 +257,25 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
 int igp_group_search_device(const double *wl, int n, const int32_t *batch, const double *hw,
                             const int32_t *grid, int n_grid, unsigned long long *best,
                             int32_t *err, void *stream);
+
+/*
+ * Request-level replay of a plan (simulate._run_workload simulate.py:98-136
+ * and the report of simulate.simulate simulate.py:139-198), constant-rate
+ * arrivals (simulate.py:75-84), n workloads with their rate, batch and
+ * predicted service time (t_inf).  seg [n+1] (device) holds segment offsets
+ * with seg[i+1] - seg[i] >= the workload's arrival count (ceil(duration *
+ * rate / 1000) + 2 is enough); lat, starts, sorted are device scratch of
+ * seg[n] doubles.  Outputs per workload: measured-latency end offsets,
+ * max queue depth, end backlog (UnstableQueueError above 10 x batch,
+ * simulate.py:163-166), measured request count, p50 / p99 (NumPy 'linear'
+ * percentile of the measured end-to-end latencies) and achieved req/s.
+ * Synchronises the stream once (to size the segmented sort).
+ */
+int igp_simulate_device(int n, const double *rate, const int32_t *batch, const double *service,
+                        double duration_ms, double warmup_ms, const int64_t *seg, double *lat,
+                        double *starts, double *sorted, int64_t *seg_end, int32_t *max_depth,
+                        int32_t *backlog, int32_t *completed, double *p50, double *p99,
+                        double *achieved, void *stream);
 
 /*
  * Solo candidate grid (BASELINE config 3): every (workload w, batch b in

@@ -18,6 +18,8 @@
 // (-fmad=false is REQUIRED: CPython rounds every multiply and add separately).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -137,6 +139,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 #define IGP_GS_MAXN 6
 #endif
 #include "exhaustive.cuh"
+#include "simulate.cuh"
 
 namespace igp {
 
@@ -874,6 +877,45 @@ int igp_group_search_device(const double *wl, int n, const int32_t *batch, const
   if (blocks > 148 * 64) blocks = 148 * 64;
   if (blocks < 1) blocks = 1;
   k_group_search<<<(unsigned)blocks, 256, 0, st>>>(G);
+  CK(cudaGetLastError());
+  return IGP_E_OK;
+}
+
+int igp_simulate_device(int n, const double *rate, const int32_t *batch, const double *service,
+                        double duration_ms, double warmup_ms, const int64_t *seg, double *lat,
+                        double *starts, double *sorted, int64_t *seg_end, int32_t *max_depth,
+                        int32_t *backlog, int32_t *completed, double *p50, double *p99,
+                        double *achieved, void *stream) {
+  if (n < 0 || !(duration_ms >= warmup_ms) || !(warmup_ms >= 0.0)) return IGP_E_ARG;
+  if (n == 0) return IGP_E_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  SimParams S;
+  S.n = n;
+  S.duration = duration_ms;
+  S.warmup = warmup_ms;
+  S.rate = rate;
+  S.batch = batch;
+  S.service = service;
+  S.seg = (const long long *)seg;
+  S.lat = lat;
+  S.starts = starts;
+  S.seg_end = (long long *)seg_end;
+  S.max_depth = max_depth;
+  S.backlog = backlog;
+  S.completed = completed;
+  k_sim_replay<<<nblk(n, 128), 128, 0, st>>>(S);
+  CK(cudaGetLastError());
+  long long total = 0;
+  CK(cudaMemcpyAsync(&total, seg + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, lat, sorted, total, n, seg, seg_end,
+                                        st));
+  void *tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, tmp_bytes > 0 ? tmp_bytes : 1, st));
+  CK(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, lat, sorted, total, n, seg, seg_end, st));
+  CK(cudaFreeAsync(tmp, st));
+  k_sim_report<<<nblk(n, 128), 128, 0, st>>>(S, sorted, p50, p99, achieved);
   CK(cudaGetLastError());
   return IGP_E_OK;
 }

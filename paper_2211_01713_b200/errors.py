@@ -64,7 +64,7 @@ class BudgetExceededError(GpuPlannerError):
 
 
 class UnstableQueueError(GpuPlannerError):
-    """Replay queue diverged (API parity only)."""
+    """Simulated queue grew beyond bound; the offered rate is not sustainable."""
 
     def __init__(self, workload: str, depth: int, bound: int):
         self.workload = workload

@@ -45,7 +45,8 @@ DEFAULT_BATCH_CAP = 32
 IGP_F_STATS = 1
 IGP_F_CTA = 4
 IGP_F_COOP = 16
-COOP_MIN_WORKLOADS = 256  # below this one warp per plan has lower latency
+CTA_MIN_WORKLOADS = 512      # one CTA per plan: 12.6 ms vs 22.5 ms (one warp) at 1k workloads
+COOP_MIN_WORKLOADS = 20_000  # whole-GPU steps: 35 us/step vs 140 (one CTA) at 100k; a tie at 10k
 
 
 @dataclass
@@ -266,7 +267,7 @@ def plan(
     wl = workload_table(workloads)
     rank = name_ranks([s.name for s, _ in workloads])
     flags = IGP_F_STATS if stats is not None else 0
-    if m >= 4096:
+    if m >= CTA_MIN_WORKLOADS:
         flags |= IGP_F_CTA  # one CTA per plan: many warps share each step's candidates
     if m >= COOP_MIN_WORKLOADS:
         # every warp of the GPU shares each step; the device falls back to the

@@ -384,6 +384,41 @@ def oracle_case(workloads, hw, budget=None, b_max=32):
     return out
 
 
+def simulate_case(workloads, hw, cfg, plan=None):
+    """The reference's simulate() (simulate.py:139-198) on a plan; the replay
+    inputs (rate, batch, predicted t_inf) are stored in report order."""
+    import importlib
+    gsim = importlib.import_module("gpuplanner.simulate")
+    out = pack_instance(workloads, hw, 32)
+    specs = {s.name: s for s, _ in workloads}
+    coefs = {s.name: c for s, c in workloads}
+    p = plan or gp.plan(workloads, hw)
+    items = []
+    for g in p.gpus:
+        pred = gp.predict_gpu(g.allocations, specs, coefs, hw)
+        for a in g.allocations:
+            items.append((a.workload, a.batch, pred[a.workload].t_inf_ms))
+    items.sort()
+    out.update(duration=np.float64(cfg.duration_ms), warmup=np.float64(cfg.warmup_ms),
+               arrival=np.array(cfg.arrival), sim_names=np.array([n for n, _, _ in items]),
+               rate=np.array([specs[n].rate_rps for n, _, _ in items]),
+               sim_batch=np.array([b for _, b, _ in items], np.int32),
+               service=np.array([t for _, _, t in items]))
+    try:
+        rep = gsim.simulate(p, specs, coefs, hw, cfg)
+    except Exception as exc:  # noqa: BLE001 - the fixture records the reference's failure
+        out.update(err_class=np.array(type(exc).__name__), err_msg=np.array(str(exc)))
+        return out
+    out.update(err_class=np.array(""), err_msg=np.array(""),
+               achieved=np.array([w.achieved_rps for w in rep.workloads]),
+               p50=np.array([w.p50_ms for w in rep.workloads]),
+               p99=np.array([w.p99_ms for w in rep.workloads]),
+               max_depth=np.array([w.max_queue_depth for w in rep.workloads], np.int32),
+               completed=np.array([w.completed for w in rep.workloads], np.int32),
+               violation=np.array([w.violation for w in rep.workloads]))
+    return out
+
+
 def stream_case(workloads, hw, b_max=32):
     out = pack_instance(workloads, hw, b_max)
     gpu_of, pos, code, units = stream_reference(workloads, hw, b_max)
@@ -393,7 +428,8 @@ def stream_case(workloads, hw, b_max=32):
 
 
 def main():
-    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream", "oracle", "document"}
+    groups = set(sys.argv[1:]) or {"plan", "component", "grid", "stream", "oracle", "document",
+                                   "simulate"}
     mpath = os.path.join(HERE, "manifest.json")
     manifest = json.load(open(mpath))["cases"] if os.path.exists(mpath) else {}
     v100 = support.make_v100()
@@ -550,6 +586,29 @@ def main():
             d = pack_instance(wls, hw, 32)
             d.update(document=np.array(json.dumps(doc)))
             save(name, d, "reference plan_to_document(plan(...)) as JSON text")
+
+    # ---- request-level replay (simulate.py:139-198), SURVEY §8f row 4 -------
+    if "simulate" in groups:
+        import importlib
+        gsim = importlib.import_module("gpuplanner.simulate")
+        twelve = support.twelve_workload_instance()
+        save("sim_c1_30s", simulate_case(twelve, v100, gsim.SimConfig(30_000.0, 1_000.0)),
+             "simulate(plan(C1), 30 s, warmup 1 s) -- SPEC acceptance 7 window")
+        inst = support.random_instance(np.random.default_rng(90), 60, v100)
+        save("sim_rand60_10s", simulate_case(inst, v100, gsim.SimConfig(10_000.0, 500.0)),
+             "simulate(plan(random_instance 60)), 10 s")
+        save("sim_rand60_nowarm", simulate_case(inst, v100, gsim.SimConfig(2_000.0)),
+             "simulate, 2 s, no warm-up")
+        save("sim_allwarm", simulate_case(twelve[:5], v100, gsim.SimConfig(500.0, 500.0)),
+             "simulate with warmup == duration (no measured requests)")
+        slow = [(gp.WorkloadSpec(f"u{i}", 40.0, 400.0, 0.5, 0.01), support.demo_coef()) for i in range(2)]
+        over = gp.Plan("manual", "v100", [gp.GpuPlan(0, [gp.Allocation("u0", 0.025, 1),
+                                                         gp.Allocation("u1", 0.025, 1)], {}, 0.95)],
+                       3.06, {})
+        save("sim_unstable", simulate_case(slow, v100, gsim.SimConfig(5_000.0), plan=over),
+             "UnstableQueueError: batch 1 at 2.5% of a device cannot keep up")
+        save("sim_poisson", simulate_case(twelve[:3], v100, gsim.SimConfig(1_000.0, arrival="poisson")),
+             "poisson arrivals: the reference's tuple seed raises TypeError on CPython 3.12")
 
     # ---- component cases ------------------------------------------------
     if "component" not in groups:
