@@ -475,6 +475,10 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.sstate = nullptr;
   P.coop = (flags & IGP_F_COOP) && n_scen == 1 ? (CoopState *)(ws + L.coop) : nullptr;
   P.win_tid = (int32_t *)(ws + L.win_tid);
+  P.sdesc = (unsigned long long *)(ws + L.sdesc);
+  P.sj = (int32_t *)(ws + L.sj);
+  P.spos = (int32_t *)(ws + L.spos);
+  P.sE = (int32_t *)(ws + L.sE);
   P.wl = wl;
   P.rank = name_rank;
   P.rank_stride = rank_stride;
@@ -733,6 +737,10 @@ static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const 
   P.sstate = (int32_t *)(ws + X.sstate);
   P.coop = nullptr;
   P.win_tid = (int32_t *)(ws + L.win_tid);
+  P.sdesc = (unsigned long long *)(ws + L.sdesc);
+  P.sj = (int32_t *)(ws + L.sj);
+  P.spos = (int32_t *)(ws + L.spos);
+  P.sE = (int32_t *)(ws + L.sE);
   P.gpu_count = (int32_t *)(ws + X.gc);
   P.stats = nullptr;
   P.err = (igp_error *)(ws + X.err);

@@ -128,7 +128,7 @@ constexpr int COOP_MAX_LANES = 160 * 512;  // lane_units rows reserved for the c
 
 struct WsLayout {
   size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
-      lane_units, sflags, perr, sched, coop, win_tid, total;
+      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, total;
   int lanes;
   int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
@@ -170,6 +170,10 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.sched = off; off = align_up(off + 4);
   L.coop = off; off = align_up(off + sizeof(CoopState));
   L.win_tid = off; off = align_up(off + ((flags & IGP_F_COOP) ? mm * 4 : 4));
+  L.sdesc = off; off = align_up(off + (size_t)S * L.gstride * 8);
+  L.sj = off; off = align_up(off + Sm * 4);
+  L.spos = off; off = align_up(off + Sm * 4);
+  L.sE = off; off = align_up(off + (size_t)S * (capx + 2) * 4);
   L.total = off;
   return L;
 }
@@ -185,6 +189,13 @@ struct PlanParams {
   int k0, k1, stream;
   int32_t *code;    // stream: per arrival error code | risk flags << 8
   int32_t *sstate;  // stream: per scenario {G, pool_top, sticky flags, arrivals}
+  // Open GPUs ordered by free units (slack = cap - occupied), descending:
+  // sj[p] / sdesc[p] = GPU index / descriptor at position p, spos[j] = the
+  // position of GPU j, sE[s] = number of GPUs with slack >= s.  A step's
+  // candidates (occupied + need <= cap, planner.py:297-299) are exactly the
+  // prefix [0, sE[need]).
+  unsigned long long *sdesc;
+  int32_t *sj, *spos, *sE;
   CoopState *coop;  // cooperative single plan: shared step state (nullable)
   int32_t *win_tid; // cooperative: thread whose lane_units hold candidate j's units
   const double *wl;     // [S][16][m]
@@ -359,6 +370,7 @@ __global__ void k_table(PlanParams P) {
 // ---------------------------------------------------------------------------
 struct GroupSmem {
   unsigned long long best;
+  int cnext;  // next candidate of the step (groups of several warps)
   unsigned long long tot[5];  // model_evals, eval calls, candidates, resident reads, started
   int err_flag;
   int win_thread;
@@ -438,6 +450,81 @@ struct ModMask {
       if ((i >> 6) == q) w[q] |= 1ull << (i & 63);
   }
 };
+
+// One warp moves GPU j (now holding desc, slack b) from slack a > b down the
+// slack order: j swaps with the last GPU of each bucket a, a-1, ..., b+1.
+// All positions come from the counts before the move, so the swaps run in
+// parallel; a bucket that is empty makes its swap a no-op.
+__device__ __forceinline__ void slack_move_down(int32_t *sj, int32_t *spos,
+                                                unsigned long long *sdesc, int32_t *sE, int j,
+                                                unsigned long long desc, int a, int b, int lane) {
+  const int steps = a - b;
+  const int p0 = spos[j];
+  __syncwarp();
+  for (int c0 = 0; c0 < steps; c0 += 32) {
+    const int i = c0 + lane;
+    int q = 0, dst = 0, xj = 0;
+    unsigned long long xd = 0;
+    if (i < steps) {
+      const int sb = a - i;
+      q = sE[sb] - 1;
+      dst = i == 0 ? p0 : sE[sb + 1] - 1;
+      xj = sj[q];
+      xd = sdesc[q];
+    }
+    __syncwarp();
+    if (i < steps && q != dst) {
+      sj[dst] = xj;
+      sdesc[dst] = xd;
+      spos[xj] = dst;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const int pf = sE[b + 1] - 1;
+    sj[pf] = j;
+    sdesc[pf] = desc;
+    spos[j] = pf;
+  }
+  __syncwarp();
+  for (int i = lane; i < steps; i += 32) sE[a - i] -= 1;
+  __syncwarp();
+}
+
+// One warp appends the new GPU j (= G, slack s) and moves it up the order:
+// it swaps with the first GPU of each bucket 0, 1, ..., s-1.
+__device__ __forceinline__ void slack_insert(int32_t *sj, int32_t *spos,
+                                             unsigned long long *sdesc, int32_t *sE, int j,
+                                             unsigned long long desc, int s, int lane) {
+  for (int c0 = 0; c0 < s; c0 += 32) {
+    const int i = c0 + lane;
+    int u = 0, dst = 0, xj = 0;
+    unsigned long long xd = 0;
+    if (i < s) {
+      u = sE[i + 1];
+      dst = i == 0 ? j : sE[i];
+      xj = sj[u];
+      xd = sdesc[u];
+    }
+    __syncwarp();
+    if (i < s && u != dst) {
+      sj[dst] = xj;
+      sdesc[dst] = xd;
+      spos[xj] = dst;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const int pf = s > 0 ? sE[s] : j;
+    sj[pf] = j;
+    sdesc[pf] = desc;
+    spos[j] = pf;
+    sE[0] = j + 1;
+  }
+  __syncwarp();
+  for (int i = lane; i < s; i += 32) sE[i + 1] += 1;
+  __syncwarp();
+}
 
 template <int MAXN>
 struct LaneArrays {  // values of residents bumped inside the current candidate
@@ -529,6 +616,8 @@ k_place(PlanParams P) {
   const double *nwt = P.nw + sm * R_NF;
   const double *tbl = P.tbl + sm * TB * 4;
   unsigned long long *gstate = P.gstate + (size_t)s * P.gstride;
+  unsigned long long *sdesc = P.sdesc + (size_t)s * P.gstride;
+  int32_t *sj = P.sj + sm, *spos = P.spos + sm, *sE = P.sE + (size_t)s * (cap + 2);
   int32_t *gcap = P.gcap + sm;
   double *gfold = P.gfold + sm * 4;
   const size_t sp = (size_t)s * (size_t)P.pool_recs;
@@ -555,6 +644,10 @@ k_place(PlanParams P) {
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
   int G = P.stream ? sst[0] : (coop_done ? P.coop->G : 0);
+  if (G == 0) {  // empty slack order
+    for (int x = COOP ? gtid : t; x < cap + 2; x += COOP ? (int)(gridDim.x * blockDim.x) : GT)
+      sE[x] = 0;
+  }
   long long tot_evals = 0, tot_calls = 0, tot_cands = 0, tot_rres = 0, tot_run = 0;
   long long st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
   int fail_code = 0;
@@ -603,10 +696,12 @@ k_place(PlanParams P) {
     if (t == 0) {
       gs.best = NO_KEY;
       gs.err_flag = 0;
+      gs.cnext = 0;
     }
     for (int x = t; x < TB * 4; x += GT) ntab[x] = tbl[(size_t)k * TB * 4 + x];
     group_sync<GW>();
     unsigned long long my_best = NO_KEY;
+    const int ncand = sE[need];  // candidates: the slack-order prefix with slack >= need
 
     // ---- the step's candidates: per-lane state machine with dynamic refill ----
     // A lane owns at most one candidate GPU.  One loop iteration advances every
@@ -619,8 +714,11 @@ k_place(PlanParams P) {
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
     auto run_step = [&](const bool serial) {
       int qhead = 0, qtail = 0;
-      int scan = serial ? 0 : (COOP ? gwarp * 64 : wi * 64);
-      const int scan_stride = serial ? 64 : (COOP ? nwarps * 64 : GT * 2);
+      int scan = 0;
+      const int scan_stride = 64;
+      // cooperative mode: this lane's next candidate position; consecutive
+      // positions go to consecutive CTAs so a step's candidates spread over all SMs
+      int c_static = (int)(threadIdx.x * gridDim.x + blockIdx.x);
       const unsigned take_mask = serial ? 1u : FULL;
       int cj = -1, c_nres = 0, c_occ = 0, c_sum = 0, c_i = 0, c_dirty = 0, c_off = 0;
       int c_pend = -1, c_pcode = 0, c_nu = 0;
@@ -680,10 +778,10 @@ k_place(PlanParams P) {
             if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[k & 1]));
             __syncwarp();
           }
-          // prefilter occupied + need <= cap (planner.py:297-299): two GPU
-          // descriptors per lane per 16-byte load; passing (j, descriptor)
-          // pairs are appended in ascending j
-          while (qtail - qhead < nidle && scan < G) {
+          // serial replay: prefilter occupied + need <= cap (planner.py:297-299)
+          // in ascending j, the reference's candidate order; two GPU
+          // descriptors per lane per 16-byte load
+          while (serial && qtail - qhead < nidle && scan < G) {
             const int jb = scan + lane * 2;
             unsigned bits = 0;
             ulonglong2 g2 = make_ulonglong2(0ull, 0ull);
@@ -714,11 +812,28 @@ k_place(PlanParams P) {
             scan += scan_stride;
           }
           __syncwarp();
+          // otherwise the step's candidates are the slack-order prefix
+          // [0, ncand): idle lanes take the next positions
+          int cbase = qhead;
+          if (!serial) {
+            if constexpr (COOP) {
+              cbase = 0;
+            } else if (GW > 1) {
+              if (lane == 0) cbase = atomicAdd(&gs.cnext, nidle);
+              cbase = __shfl_sync(FULL, cbase, 0);
+            }
+          }
           if ((idle >> lane) & 1u) {
             const int r = __popc(idle & lt);
-            if (qhead + r < qtail) {
-              const int j = q[(qhead + r) & (QN - 1)];
-              const unsigned long long g = qg[(qhead + r) & (QN - 1)];
+            int cpos = cbase + r;
+            if (COOP && !serial) {
+              cpos = c_static;
+              c_static += (int)(gridDim.x * blockDim.x);
+            }
+            const bool have = serial ? (qhead + r < qtail) : (cpos < ncand);
+            if (have) {
+              const int j = serial ? q[(qhead + r) & (QN - 1)] : sj[cpos];
+              const unsigned long long g = serial ? qg[(qhead + r) & (QN - 1)] : sdesc[cpos];
               st_cands += 1;
               const volatile unsigned long long *bp = &gs.best;
               if (exact || ((((unsigned long long)need) << 32) | (unsigned)j) <= *bp) {
@@ -770,12 +885,17 @@ k_place(PlanParams P) {
               }
             }
           }
-          qhead = min(qtail, qhead + nidle);
+          qhead = serial ? min(qtail, qhead + nidle) : qhead + nidle;
           __syncwarp();
         }
         const unsigned busy = __ballot_sync(FULL, cj >= 0);
         if (!busy) {
-          if (qhead >= qtail && scan >= G) break;
+          bool more;
+          if (serial) more = qhead < qtail || scan < G;
+          else if (COOP) more = __any_sync(FULL, c_static < ncand);
+          else if (GW > 1) more = *(volatile int *)&gs.cnext < ncand;
+          else more = qhead < ncand;
+          if (!more) break;
           continue;
         }
         if (cj < 0) continue;
@@ -1098,11 +1218,15 @@ k_place(PlanParams P) {
             }
           }
         }
+        __syncwarp();
+        if (*(volatile int *)abortp == 0)
+          slack_insert(sj, spos, sdesc, sE, G, gstate[G], cap - need, lane);
       } else {
         const int j = (int)(bk & 0xffffffffu);
         const int wt = COOP ? P.win_tid[j] : gs.win_thread;
         const uint16_t *lu = lane_units + (size_t)wt * cap;
         const int nres = (int)((gstate[j] >> 16) & 0xffffu);
+        const int occ_old = (int)(gstate[j] & 0xffffu);
         const int n = nres + 1;
         int off = (int)(gstate[j] >> 32);
         const int tcap = gcap[j];
@@ -1202,6 +1326,10 @@ k_place(PlanParams P) {
               P.pos[sm + k] = nres;
             }
           }
+          __syncwarp();
+          slack_move_down(sj, spos, sdesc, sE, j,
+                          ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16),
+                          cap - occ_old, cap - part, lane);
         }
       }
     }
