@@ -46,7 +46,7 @@ IGP_F_STATS = 1
 IGP_F_CTA = 4
 IGP_F_COOP = 16
 CTA_MIN_WORKLOADS = 512      # one CTA per plan: 12.6 ms vs 22.5 ms (one warp) at 1k workloads
-COOP_MIN_WORKLOADS = 20_000  # whole-GPU steps: 35 us/step vs 140 (one CTA) at 100k; a tie at 10k
+COOP_MIN_WORKLOADS = 5_000  # whole-GPU steps: 17.5 vs 20.1 us/step (one CTA) at 10k, 21 vs 157 at 100k
 
 
 @dataclass
