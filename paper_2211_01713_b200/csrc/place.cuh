@@ -53,7 +53,6 @@ struct Meta {
 #endif
 constexpr int SLOT = IGP_SLOT;
 constexpr int SLOT_META = (SLOT + 1) & ~1;
-constexpr int QN = 128;  // per-warp candidate ring queue
 
 struct __align__(16) LaneSlot {
   double rec[SLOT][R_NF];
@@ -549,17 +548,18 @@ k_place(PlanParams P) {
   constexpr unsigned long long NO_KEY = ~0ull;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ GroupSmem gsm[GPB];
-  __shared__ int qsm[GPB * GW][QN];
-  __shared__ unsigned long long qgs[GPB * GW][QN];
-  __shared__ double ntb[GPB][TB * 4];  // the newcomer's solo table row
+  __shared__ __align__(16) double ntb[GPB][TB * 4];  // the newcomer's solo table row
+  __shared__ unsigned long long nbar[GPB];          // its bulk copy's mbarrier
   extern __shared__ __align__(16) unsigned char dsm[];
   const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
   GroupSmem &gs = gsm[grp];
   LaneSlot *const sl = reinterpret_cast<LaneSlot *>(dsm) + threadIdx.x;
   mbar_init(&sl->mbar);
+  if (t == 0) mbar_init(&nbar[grp]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   uint32_t c_phase = 0;  // parity of this lane's mbarrier
+  uint32_t n_phase = 0;  // parity of the group's newcomer-row mbarrier
   CoopState *const cs = P.coop;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;      // cooperative lane id
   const int gwarp = gtid >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -577,8 +577,6 @@ k_place(PlanParams P) {
     group_sync<GW>();
     if (s >= P.S) break;
   }
-  int *q = qsm[grp * GW + wi];
-  unsigned long long *qg = qgs[grp * GW + wi];
   double *ntab = ntb[grp];
   const Hw &hw = P.hw;
   const int m = P.m, cap = hw.cap;
@@ -698,7 +696,12 @@ k_place(PlanParams P) {
       gs.err_flag = 0;
       gs.cnext = 0;
     }
-    for (int x = t; x < TB * 4; x += GT) ntab[x] = tbl[(size_t)k * TB * 4 + x];
+    if (t == 0) {  // the newcomer's solo row: waited for only by a newcomer bump
+      fence_async_smem();  // last step's reads of ntab before the async overwrite
+      mbar_expect_tx(&nbar[grp], TB * 32);
+      bulk_g2s(ntab, tbl + (size_t)k * TB * 4, TB * 32, &nbar[grp]);
+    }
+    bool n_ready = false;
     group_sync<GW>();
     unsigned long long my_best = NO_KEY;
     const int ncand = sE[need];  // candidates: the slack-order prefix with slack >= need
@@ -713,9 +716,8 @@ k_place(PlanParams P) {
     // candidate.  serial != 0 replays the step in the reference's order on
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
     auto run_step = [&](const bool serial) {
-      int qhead = 0, qtail = 0;
-      int scan = 0;
-      const int scan_stride = 64;
+      int qhead = 0;
+      int scan = 0;  // serial replay: next GPU index to test
       // cooperative mode: this lane's next candidate position; consecutive
       // positions go to consecutive CTAs so a step's candidates spread over all SMs
       int c_static = (int)(threadIdx.x * gridDim.x + blockIdx.x);
@@ -778,42 +780,8 @@ k_place(PlanParams P) {
             if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[k & 1]));
             __syncwarp();
           }
-          // serial replay: prefilter occupied + need <= cap (planner.py:297-299)
-          // in ascending j, the reference's candidate order; two GPU
-          // descriptors per lane per 16-byte load
-          while (serial && qtail - qhead < nidle && scan < G) {
-            const int jb = scan + lane * 2;
-            unsigned bits = 0;
-            ulonglong2 g2 = make_ulonglong2(0ull, 0ull);
-            if (jb < G) {
-              g2 = *reinterpret_cast<const ulonglong2 *>(gstate + jb);
-              const int lim = cap - need;
-              bits = ((int)(g2.x & 0xffffu) <= lim ? 1u : 0u) |
-                     ((jb + 1 < G && (int)(g2.y & 0xffffu) <= lim) ? 2u : 0u);
-            }
-            const int cnt = __popc(bits);
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int v = __shfl_up_sync(FULL, incl, o);
-              if (lane >= o) incl += v;
-            }
-            int qp = qtail + incl - cnt;
-            if (bits & 1u) {
-              q[qp & (QN - 1)] = jb;
-              qg[qp & (QN - 1)] = g2.x;
-              ++qp;
-            }
-            if (bits & 2u) {
-              q[qp & (QN - 1)] = jb + 1;
-              qg[qp & (QN - 1)] = g2.y;
-            }
-            qtail += __shfl_sync(FULL, incl, 31);
-            scan += scan_stride;
-          }
-          __syncwarp();
-          // otherwise the step's candidates are the slack-order prefix
-          // [0, ncand): idle lanes take the next positions
+          // the step's candidates are the slack-order prefix [0, ncand): idle
+          // lanes take the next positions
           int cbase = qhead;
           if (!serial) {
             if constexpr (COOP) {
@@ -830,10 +798,27 @@ k_place(PlanParams P) {
               cpos = c_static;
               c_static += (int)(gridDim.x * blockDim.x);
             }
-            const bool have = serial ? (qhead + r < qtail) : (cpos < ncand);
+            int j = 0;
+            unsigned long long g = 0;
+            bool have;
+            if (serial) {
+              // the serial replay (lane 0 only) follows the reference's candidate
+              // order: ascending j through the prefilter (planner.py:296-299)
+              while (scan < G && (int)(gstate[scan] & 0xffffu) + need > cap) ++scan;
+              have = scan < G;
+              if (have) {
+                j = scan;
+                g = gstate[scan];
+                ++scan;
+              }
+            } else {
+              have = cpos < ncand;
+              if (have) {
+                j = sj[cpos];
+                g = sdesc[cpos];
+              }
+            }
             if (have) {
-              const int j = serial ? q[(qhead + r) & (QN - 1)] : sj[cpos];
-              const unsigned long long g = serial ? qg[(qhead + r) & (QN - 1)] : sdesc[cpos];
               st_cands += 1;
               const volatile unsigned long long *bp = &gs.best;
               if (exact || ((((unsigned long long)need) << 32) | (unsigned)j) <= *bp) {
@@ -885,13 +870,13 @@ k_place(PlanParams P) {
               }
             }
           }
-          qhead = serial ? min(qtail, qhead + nidle) : qhead + nidle;
+          qhead += nidle;
           __syncwarp();
         }
         const unsigned busy = __ballot_sync(FULL, cj >= 0);
         if (!busy) {
           bool more;
-          if (serial) more = qhead < qtail || scan < G;
+          if (serial) more = __shfl_sync(FULL, scan, 0) < G;
           else if (COOP) more = __any_sync(FULL, c_static < ncand);
           else if (GW > 1) more = *(volatile int *)&gs.cnext < ncand;
           else more = qhead < ncand;
@@ -1048,6 +1033,10 @@ k_place(PlanParams P) {
             c_nu += 1;
             const int v = c_nu - need;
             if (v < TB && c_nu <= cap) {
+              if (!n_ready) {
+                mbar_wait(&nbar[grp], n_phase);
+                n_ready = true;
+              }
               const double *tv = ntab + v * 4;
               so.ka = tv[0];
               so.pw = tv[1];
@@ -1115,6 +1104,9 @@ k_place(PlanParams P) {
 
     run_step(false);
     group_sync<GW>();
+    if (t == 0 && !n_ready) mbar_wait(&nbar[grp], n_phase);  // retire this step's row copy
+    n_ready = true;
+    n_phase ^= 1u;
 
     if (gs.err_flag) {
       // exact mode only: replay the step in the reference's candidate order to
