@@ -81,7 +81,7 @@ def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
     return int(lib.igp_plan_workspace_bytes(S, m, _np_ptr(h), b_max, flags))
 
 
-POOL_RETRY = 12  # 8*G + 4*m <= 12*m records always suffice (csrc/place.cuh)
+POOL_RETRY = 14  # tiles 4m + 8G <= 12m records plus <= 2m header slots always suffice
 
 
 def plan_device(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True):

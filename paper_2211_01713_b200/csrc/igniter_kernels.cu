@@ -429,6 +429,9 @@ static int launch_place_coop(PlanParams P, cudaStream_t st) {
   const int lim = want_ctas ? want_ctas : (by_m > 1 ? by_m : 1);
   if (grid > lim) grid = lim;
   CK(cudaMemsetAsync(P.coop, 0, sizeof(CoopState), st));
+  // the slack order starts empty before any warp reads it (the kernel has no
+  // grid-wide barrier before its first step)
+  CK(cudaMemsetAsync(P.sE, 0, sizeof(int32_t) * (P.hw.cap + 2), st));
   CK(cudaMemsetAsync(P.coop->best, 0xff, sizeof(P.coop->best), st));
   void *args[] = {&P};
   CK(cudaLaunchCooperativeKernel((const void *)k_place<MAXN, 1, true>, dim3(grid), dim3(128), args,

@@ -52,12 +52,23 @@ struct Meta {
 #define IGP_SLOT 3
 #endif
 constexpr int SLOT = IGP_SLOT;
-constexpr int SLOT_META = (SLOT + 1) & ~1;
+static_assert(SLOT >= 1 && SLOT <= 4, "the tile header carries the first four residents' meta");
+
+// A tile in the record pool is one header record followed by the resident
+// records; the header mirrors the GPU's Neumaier fold state and the first
+// residents' meta, so one bulk copy stages everything a candidate reads.
+struct __align__(16) TileHeader {
+  double gf[4];  // Neumaier (s, c) of the power and cache sums over residents
+  Meta meta[4];  // (workload, units, lower bound) of residents 0..3
+  double pad[4];
+};
+static_assert(sizeof(TileHeader) == R_NF * 8, "the header occupies one record slot");
 
 struct __align__(16) LaneSlot {
-  double rec[SLOT][R_NF];
-  Meta meta[SLOT_META];
-  double gf[4];
+  double gf[4];  // staged header ...
+  Meta meta[4];
+  double hpad[4];
+  double rec[SLOT][R_NF];  // ... and the first SLOT resident records
   unsigned long long mbar;
   unsigned long long pad;
 };
@@ -137,7 +148,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int pool_factor(int flags) {
   const int f = (flags >> 8) & 0xff;
-  return f ? f : 6;
+  return f ? f : 7;
 }
 
 static WsLayout ws_layout(int S, int m, int cap, int flags) {
@@ -642,9 +653,8 @@ k_place(PlanParams P) {
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
   int G = P.stream ? sst[0] : (coop_done ? P.coop->G : 0);
-  if (G == 0) {  // empty slack order
-    for (int x = COOP ? gtid : t; x < cap + 2; x += COOP ? (int)(gridDim.x * blockDim.x) : GT)
-      sE[x] = 0;
+  if (!COOP && G == 0) {  // empty slack order (the cooperative launch zeroes it on the host side)
+    for (int x = t; x < cap + 2; x += GT) sE[x] = 0;
   }
   long long tot_evals = 0, tot_calls = 0, tot_cands = 0, tot_rres = 0, tot_run = 0;
   long long st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
@@ -829,15 +839,12 @@ k_place(PlanParams P) {
                 c_off = (int)(g >> 32);
                 st_rres += c_nres;
                 st_run += 1;
-                {  // stage the resident tile: one bulk copy group per candidate
+                {  // stage the tile header and the first SLOT records: one bulk copy
                   const int nst = c_nres < SLOT ? c_nres : SLOT;
-                  const uint32_t brec = (uint32_t)nst * (R_NF * 8);
-                  const uint32_t bmeta = (uint32_t)((nst + 1) >> 1) * 16u;
+                  const uint32_t bytes = (uint32_t)(1 + nst) * (R_NF * 8);
                   fence_async_smem();
-                  mbar_expect_tx(&sl->mbar, brec + bmeta + 32u);
-                  bulk_g2s(sl->rec, rec + (size_t)c_off * R_NF, brec, &sl->mbar);
-                  bulk_g2s(sl->meta, meta + c_off, bmeta, &sl->mbar);
-                  bulk_g2s(sl->gf, gfold + (size_t)j * 4, 32u, &sl->mbar);
+                  mbar_expect_tx(&sl->mbar, bytes);
+                  bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, &sl->mbar);
                   c_wait = true;
                 }
                 c_sum = c_occ + need;
@@ -1168,7 +1175,7 @@ k_place(PlanParams P) {
     if (committer) {
       if (bk == NO_KEY) {
         if (lane == 0) {
-          const int off = *poolp;
+          const int off = *poolp + 1;  // records after the header slot
           if (off + TILE0 > P.pool_recs) {
             *abortp = IGP_E_CAPACITY;
           } else {
@@ -1204,6 +1211,12 @@ k_place(PlanParams P) {
             gf[1] = fp.c;
             gf[2] = fc.s;
             gf[3] = fc.c;
+            TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
+            hd->gf[0] = fp.s;
+            hd->gf[1] = fp.c;
+            hd->gf[2] = fc.s;
+            hd->gf[3] = fc.c;
+            hd->meta[0] = meta[off];
             if (P.stream) {
               P.gpu_of[sm + k] = G;
               P.pos[sm + k] = 0;
@@ -1225,7 +1238,7 @@ k_place(PlanParams P) {
         if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
           int noff = 0;
           if (lane == 0) {
-            noff = *poolp;
+            noff = *poolp + 1;  // records after the header slot
             if (noff + 2 * tcap > P.pool_recs) *abortp = IGP_E_CAPACITY;
             else *poolp = noff + 2 * tcap;
           }
@@ -1313,6 +1326,12 @@ k_place(PlanParams P) {
             gf[1] = fp.c;
             gf[2] = fc.s;
             gf[3] = fc.c;
+            TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
+            hd->gf[0] = fp.s;
+            hd->gf[1] = fp.c;
+            hd->gf[2] = fc.s;
+            hd->gf[3] = fc.c;
+            for (int r = 0; r < n && r < 4; ++r) hd->meta[r] = meta[off + r];
             if (P.stream) {
               P.gpu_of[sm + k] = j;
               P.pos[sm + k] = nres;
