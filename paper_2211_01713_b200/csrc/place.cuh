@@ -99,21 +99,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t phas
       "r"(phase)
       : "memory");
 }
-// non-blocking completion test of the phase with the given parity
-__device__ __forceinline__ bool mbar_test(unsigned long long *bar, uint32_t phase) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
-      : "memory");
-  return ok != 0;
-}
-// bulk prefetch into L2 (no shared memory, no completion to wait for)
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // generic-proxy writes -> later async-proxy (TMA) access of the same memory
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
