@@ -558,7 +558,6 @@ k_place(PlanParams P) {
   uint32_t n_phase = 0;  // parity of the group's newcomer-row mbarrier
   CoopState *const cs = P.coop;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;      // cooperative lane id
-  const int gwarp = gtid >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   // Persistent groups: each pulls the next scenario when it finishes one, so
   // scenarios of unequal length do not leave SMs idle at the end.
   for (int pass = 0;; ++pass) {
