@@ -1245,11 +1245,20 @@ k_place(PlanParams P) {
         if (*(volatile int *)abortp == 0) {
           const double dnext = delta_sch(hw, n + 1);
           int part = 0;
+          // fold inputs and meta of resident `lane`, handed to the prefix fold
+          // below by shuffles instead of re-reading them from the pool
+          double f_pw = 0.0, f_ca = 0.0;
+          unsigned long long f_mt = 0ull;
           for (int r = lane; r < n; r += 32) {
             const int nu = lu[r];
             double *rr = rec + (size_t)(off + r) * R_NF;
             if (r < nres) {
               Meta mt = meta[off + r];
+              if (nu == (int)mt.u && r < 32) {
+                const double2 fv = *reinterpret_cast<const double2 *>(frec + (size_t)(off + r) * 2);
+                f_pw = fv.x;
+                f_ca = fv.y;
+              }
               if (nu != (int)mt.u) {
                 const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
                 const Solo s1 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu + 1);
@@ -1264,7 +1273,12 @@ k_place(PlanParams P) {
                 frec[(size_t)(off + r) * 2 + 1] = so.ca;
                 mt.u = (uint16_t)nu;
                 meta[off + r] = mt;
+                if (r < 32) {
+                  f_pw = so.pw;
+                  f_ca = so.ca;
+                }
               }
+              if (r < 32) f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
               const double *ce = cold + (size_t)mt.k * C_NF;
               rr[R_TSN] = (ce[C_KSCH] + dnext) * ce[C_NK];
             } else {
@@ -1285,26 +1299,46 @@ k_place(PlanParams P) {
               rr[R_THALF] = nw_thalf;
               frec[(size_t)(off + r) * 2] = so.pw;
               frec[(size_t)(off + r) * 2 + 1] = so.ca;
-              meta[off + r] = Meta{k, (uint16_t)nu, (uint16_t)need};
+              const Meta mt{k, (uint16_t)nu, (uint16_t)need};
+              meta[off + r] = mt;
+              if (r < 32) {
+                f_pw = so.pw;
+                f_ca = so.ca;
+                f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
+              }
             }
             part += nu;
           }
           part = warp_sum(part);
           __syncwarp();
-          if (lane == 0) {
-            gstate[j] = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
-            // prefix fold states of this GPU, in resident order
-            Neumaier fp, fc;
-            fp.s = fp.c = fc.s = fc.c = 0.0;
-            for (int r = 0; r < n; ++r) {
+          // prefix fold states of this GPU, in resident order (every lane folds
+          // the shuffled terms identically; lane 0 stores them)
+          Neumaier fp, fc;
+          fp.s = fp.c = fc.s = fc.c = 0.0;
+          for (int r = 0; r < n; ++r) {
+            double pw, ca;
+            if (r < 32) {
+              pw = __shfl_sync(FULL, f_pw, r);
+              ca = __shfl_sync(FULL, f_ca, r);
+            } else {
+              pw = frec[(size_t)(off + r) * 2];
+              ca = frec[(size_t)(off + r) * 2 + 1];
+            }
+            if (lane == 0) {
               double *pp = pfx + (size_t)(off + r) * 4;
               pp[0] = fp.s;
               pp[1] = fp.c;
               pp[2] = fc.s;
               pp[3] = fc.c;
-              fp.add(frec[(size_t)(off + r) * 2]);
-              fc.add(frec[(size_t)(off + r) * 2 + 1]);
             }
+            fp.add(pw);
+            fc.add(ca);
+          }
+          unsigned long long hmeta[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) hmeta[r] = __shfl_sync(FULL, f_mt, r);
+          if (lane == 0) {
+            gstate[j] = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
             double *gf = gfold + (size_t)j * 4;
             gf[0] = fp.s;
             gf[1] = fp.c;
@@ -1315,7 +1349,8 @@ k_place(PlanParams P) {
             hd->gf[1] = fp.c;
             hd->gf[2] = fc.s;
             hd->gf[3] = fc.c;
-            for (int r = 0; r < n && r < 4; ++r) hd->meta[r] = meta[off + r];
+            for (int r = 0; r < n && r < 4; ++r)
+              *reinterpret_cast<unsigned long long *>(&hd->meta[r]) = hmeta[r];
             if (P.stream) {
               P.gpu_of[sm + k] = j;
               P.pos[sm + k] = nres;
