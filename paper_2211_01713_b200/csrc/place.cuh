@@ -365,7 +365,6 @@ __global__ void k_table(PlanParams P) {
 // ---------------------------------------------------------------------------
 struct GroupSmem {
   unsigned long long best;
-  int cnext;  // next candidate of the step (groups of several warps)
   unsigned long long tot[5];  // model_evals, eval calls, candidates, resident reads, started
   int err_flag;
   int win_thread;
@@ -688,7 +687,6 @@ k_place(PlanParams P) {
     if (t == 0) {
       gs.best = NO_KEY;
       gs.err_flag = 0;
-      gs.cnext = 0;
     }
     if (t == 0) {  // the newcomer's solo row: waited for only by a newcomer bump
       fence_async_smem();  // last step's reads of ntab before the async overwrite
@@ -780,14 +778,13 @@ k_place(PlanParams P) {
           if (!serial) {
             if constexpr (COOP) {
               cbase = 0;
-            } else if (GW > 1) {
-              if (lane == 0) cbase = atomicAdd(&gs.cnext, nidle);
-              cbase = __shfl_sync(FULL, cbase, 0);
             }
           }
           if ((idle >> lane) & 1u) {
             const int r = __popc(idle & lt);
-            int cpos = cbase + r;
+            // several warps per scenario: positions interleave over the warps,
+            // so a step's few candidates spread out instead of filling one warp
+            int cpos = GW > 1 ? wi + GW * (cbase + r) : cbase + r;
             if (COOP && !serial) {
               cpos = c_static;
               c_static += (int)(gridDim.x * blockDim.x);
@@ -869,7 +866,7 @@ k_place(PlanParams P) {
           bool more;
           if (serial) more = __shfl_sync(FULL, scan, 0) < G;
           else if (COOP) more = __any_sync(FULL, c_static < ncand);
-          else if (GW > 1) more = *(volatile int *)&gs.cnext < ncand;
+          else if (GW > 1) more = wi + GW * qhead < ncand;
           else more = qhead < ncand;
           if (!more) break;
           continue;
