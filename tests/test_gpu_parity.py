@@ -126,8 +126,11 @@ def _compare_to_oracle(res, s, wl, hw_vec, b_max, rank, oracle, stats=False):
     return o
 
 
-@pytest.mark.parametrize("flags", [0, IGP_F_STATS, IGP_F_CTA, IGP_F_CTA | IGP_F_STATS])
+@pytest.mark.parametrize("flags", [0, IGP_F_STATS, IGP_F_CTA, IGP_F_CTA | IGP_F_STATS, 32, 64,
+                                   64 | IGP_F_STATS])
 def test_scenario_batch_vs_oracle(oracle_lib, flags):
+    """Scenario batches in every group width: one warp (default), two / four
+    warps (IGP_F_GW2 = 32, IGP_F_GW4 = 64) and one CTA per scenario."""
     hw = make_v100()
     rng = np.random.default_rng(123)
     scen = [random_instance(rng, 300, hw) for _ in range(12)]
