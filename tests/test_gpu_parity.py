@@ -307,3 +307,52 @@ def test_plan_document_matches_reference_text(case):
     assert rev == doc
     allocs = allocations_from_document(doc)
     assert sum(len(a) for a in allocs) == len(wls)
+
+
+def _random_states(rng, n_states, nmax, r_unit, floor=False):
+    """Random device states over wide coefficient ranges (test_model_properties.py
+    ranges), half of them at unit multiples, the rest at arbitrary r."""
+    counts = rng.integers(1, nmax + 1, n_states)
+    n = int(counts.sum())
+    wl = np.empty((16, n))
+    wl[0] = rng.uniform(1.0, 200.0, n)
+    wl[1] = rng.uniform(1.0, 2000.0, n)
+    wl[2] = rng.uniform(0.0, 2.0, n)
+    wl[3] = rng.uniform(0.0, 0.5, n)
+    wl[4] = rng.integers(1, 501, n)
+    wl[5] = rng.uniform(0.0, 0.01, n)
+    wl[6] = rng.uniform(0.0, 0.02, n)
+    wl[7] = rng.uniform(0.0, 0.2, n)
+    wl[8] = rng.uniform(0.0, 20.0, n)
+    wl[9] = rng.uniform(0.0, 2.0, n)
+    wl[10] = rng.uniform(1e-3, 1.0, n)
+    wl[11] = rng.uniform(0.0, 2000.0 if floor else 100.0, n)
+    wl[12] = rng.uniform(0.0, 400.0 if floor else 200.0, n)
+    wl[13] = rng.uniform(0.0, 0.2, n)
+    wl[14] = rng.uniform(0.0, 0.5, n)
+    wl[15] = rng.uniform(0.0, 1.0, n)
+    batch = rng.integers(1, 129, n).astype(np.int32)
+    u = rng.integers(1, int(round(1.0 / r_unit)) + 1, n)
+    r = np.where(rng.random(n) < 0.5, u * r_unit, rng.uniform(0.001, 1.0, n))
+    ptr = np.zeros(n_states + 1, np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    return wl, batch, r, ptr
+
+
+@pytest.mark.parametrize("r_unit,nmax,floor", [(0.025, 12, False), (0.01, 30, False),
+                                               (0.025, 8, True)])
+def test_eval_states_million_random_states_vs_oracle(oracle_lib, r_unit, nmax, floor):
+    """_eval_entries rows bit-equal on >= 1e6 random
+    device states (n = 1..nmax; cap binding, f_min floor and clamps included)."""
+    rng = np.random.default_rng(int(r_unit * 1000) + nmax)
+    n_states = 1_000_000 if not floor else 200_000
+    wl, batch, r, ptr = _random_states(rng, n_states, nmax, r_unit, floor)
+    hw = np.array(hw_vector(make_v100(r_unit=r_unit)))
+    rows, err = _device.eval_states(wl, batch, r, ptr, hw)
+    orows, rc = oracle_lib.eval_states(wl, batch, r, ptr, hw)
+    assert rc == 0 and (err["code"] == 0).all()
+    np.testing.assert_array_equal(G.bits(rows), G.bits(orows))
+    f = rows[:, 3]
+    assert (f < hw[1]).mean() > 0.1  # the power cap binds in a good share of states
+    if floor:
+        assert (f == hw[10] * hw[1]).mean() > 0.1  # f_min floor reached

@@ -100,3 +100,21 @@ def test_oracle_stream_matches_reference_driver(oracle_lib, case):
     for k in ("gpu_of", "pos", "code", "units"):
         np.testing.assert_array_equal(o[k], d[k], err_msg=k)
     assert o["gpu_count"] == int(d["gpu_count"])
+
+
+def test_plan_document_roundtrip_helpers(tmp_path):
+    """allocations_from_document / write_json_atomic on the reference's own
+    document text (problem.py:344-398)."""
+    import json
+    from paper_2211_01713_b200.document import allocations_from_document, write_json_atomic
+    from paper_2211_01713_b200.errors import ProblemFormatError
+    d = G.load("doc_c1_twelve")
+    doc = json.loads(str(d["document"]))
+    allocs = allocations_from_document(doc)
+    assert [len(a) for a in allocs] == [len(g["allocations"]) for g in doc["gpus"]]
+    assert allocs[0][0].workload == doc["gpus"][0]["allocations"][0]["workload"]
+    path = tmp_path / "sub" / "plan.json"
+    write_json_atomic(path, doc)
+    assert json.loads(path.read_text()) == doc
+    with pytest.raises(ProblemFormatError, match="missing required field 'gpus'"):
+        allocations_from_document({})
