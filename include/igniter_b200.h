@@ -223,6 +223,9 @@ int igp_prologue_device(const double *wl, int m, const double *hw, int b_max,
  * tracks k0 = arrivals pushed so far.
  *   push:      wl_new [S][16][n]; outputs [S][n]: GPU index and position
  *              within that GPU at admission (-1 when rejected), and the code
+ *              (IGP_E_* in the low 8 bits); err [S] (device, nullable): a
+ *              stream whose record pool overflowed reports IGP_E_CAPACITY
+ *              and stops admitting until it is reset with a larger pool
  *   snapshot:  [S][n_arrivals] current GPU, position and units of every
  *              arrival (units 0 when rejected), breakdown rows (nullable),
  *              GPU count and the predict_gpu error record per stream
@@ -233,7 +236,7 @@ int igp_stream_reset_device(int n_streams, int capacity, const double *hw, int b
                             void *workspace, size_t workspace_bytes, int flags, void *stream);
 int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, int capacity,
                            const double *hw, int b_max, int32_t *gpu_of, int32_t *pos,
-                           int32_t *code, int64_t *stats, void *workspace,
+                           int32_t *code, int64_t *stats, igp_error *err, void *workspace,
                            size_t workspace_bytes, int flags, void *stream);
 int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, const double *hw,
                                int b_max, int32_t *gpu_of, int32_t *pos, int32_t *units,

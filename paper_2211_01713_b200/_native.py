@@ -98,8 +98,8 @@ PROTOTYPES = {
                                  _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "igp_stream_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I]),
     "igp_stream_reset_device": (_I, [_I, _I, _VP, _I, _VP, _SZ, _I, _VP]),
-    "igp_stream_push_device": (_I, [_VP, _I, _I, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _SZ,
-                                    _I, _VP]),
+    "igp_stream_push_device": (_I, [_VP, _I, _I, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _VP,
+                                    _SZ, _I, _VP]),
     "igp_stream_snapshot_device": (_I, [_I, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                         _SZ, _I, _VP]),
 }

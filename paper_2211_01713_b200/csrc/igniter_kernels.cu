@@ -770,7 +770,7 @@ int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int
 
 int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, int capacity,
                            const double *hw_h, int b_max, int32_t *gpu_of, int32_t *pos,
-                           int32_t *code, int64_t *stats, void *workspace,
+                           int32_t *code, int64_t *stats, igp_error *err, void *workspace,
                            size_t workspace_bytes, int flags, void *stream) {
   if (n_streams < 1 || capacity < 1 || k0 < 0 || n < 0 || k0 + n > capacity || !hw_h ||
       !workspace)
@@ -810,6 +810,8 @@ int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, i
   if (code)
     CK(cudaMemcpy2DAsync(code, sp, ws + X.code + (size_t)k0 * 4, dp, sp, S,
                          cudaMemcpyDeviceToDevice, st));
+  if (err)
+    CK(cudaMemcpyAsync(err, ws + X.err, S * sizeof(igp_error), cudaMemcpyDeviceToDevice, st));
   return IGP_E_OK;
 }
 

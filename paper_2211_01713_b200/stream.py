@@ -46,6 +46,8 @@ class StreamPlanner:
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._out = torch.empty((3, self.S, self.C), dtype=torch.int32, device=self.device)
         self.stats = torch.zeros((self.S, 6), dtype=torch.int64, device=self.device)
+        self.err = torch.zeros((self.S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8,
+                               device=self.device)
         self.reset()
 
     def _stream(self):
@@ -71,8 +73,8 @@ class StreamPlanner:
         rc = self.lib.igp_stream_push_device(
             _device._ptr(wl_new), self.S, self.k, n, self.C, _device._np_ptr(self.hv), self.b_max,
             _device._ptr(out[0]), _device._ptr(out[1]), _device._ptr(out[2]),
-            _device._ptr(self.stats), _device._ptr(self.ws), self.ws.numel(), self.flags,
-            self._stream())
+            _device._ptr(self.stats), _device._ptr(self.err), _device._ptr(self.ws),
+            self.ws.numel(), self.flags, self._stream())
         _device._check(rc)
         self.k += n
         return out[0], out[1], out[2]
@@ -87,7 +89,17 @@ class StreamPlanner:
             d = torch.from_numpy(wl_new).to(self.device)
             g, p, c = self.push_device(d)
             g, p, c = (x.cpu().numpy().copy() for x in (g, p, c))
+            self.check_errors()
         return dict(gpu_of=g, pos=p, code=c & 0xFF)
+
+    def check_errors(self):
+        """Raise if a stream's device state broke (record pool overflow)."""
+        codes = self.err.cpu().numpy().view(_native.err_dtype()).reshape(self.S)["code"]
+        if (codes != 0).any():
+            from .errors import NativeError
+            bad = int(np.nonzero(codes)[0][0])
+            raise NativeError(f"stream {bad}: device state error {int(codes[bad])} "
+                              "(record pool exhausted: recreate with a larger pool factor)")
 
     def push(self, workloads):
         """Append one arrival list per stream (lists of equal length of

@@ -83,3 +83,15 @@ def test_stream_r_unit_001_b128_vs_oracle(oracle_lib):
         o = oracle_lib.stream(wl[s], np.array(hw_vector(hw)), 128)
         np.testing.assert_array_equal(r["gpu_of"][s], o["gpu_of"])
         np.testing.assert_array_equal(snap["units"][s], o["units"])
+
+
+def test_stream_pool_overflow_is_reported():
+    """A stream whose record pool runs out (pool factor 1 via flags bits 8..15)
+    reports it instead of silently dropping arrivals."""
+    from instances import make_v100
+    from paper_2211_01713_b200.errors import NativeError
+    hw = make_v100()
+    wl, _ = synth.scenarios(1, 600, hw, seed=79)
+    sp = StreamPlanner(hw, capacity=600, flags=1 << 8)
+    with pytest.raises(NativeError, match="record pool"):
+        sp.push_arrays(wl)
