@@ -128,7 +128,13 @@ def c2():
         dp = DevicePlan(wl, hv, 32, rk, fl)
         out[tag] = dp.time(10)
     st = dp.ref_stats()
+    from oracle import oracle
+    t0 = time.perf_counter()
+    for _ in range(5):
+        oracle.plan(wl[0], hv, 32, rk)
+    cpu_ms = (time.perf_counter() - t0) / 5 * 1e3
     emit(dict(config="C2", workload="1 plan of 1,000 synthetic workloads, r_unit 0.025, b<=32",
+              cpu_oracle_ms_per_plan_1core=cpu_ms,
               ms_per_plan_warp=out["warp"], ms_per_plan_cta=out["cta"],
               ms_per_plan_coop=out["coop"],
               us_per_step=min(out.values()) * 1e3 / 1000, reference_counters=st,
@@ -146,7 +152,14 @@ def c3():
     dp = DevicePlan(wl, hv, 128, rk, IGP_F_CTA | IGP_F_COOP)
     plan_ms = dp.time(1)
     st = dp.ref_stats()
-    emit(dict(config="C3-plan", workload="1 plan of 100,000 workloads, r_unit 0.01, b<=128 "
+    from oracle import oracle
+    sub = np.ascontiguousarray(wl[0][:, :10_000])
+    t0 = time.perf_counter()
+    o = oracle.plan(sub, hv, 128, name_ranks(list(names[:10_000])))
+    cpu_sub = time.perf_counter() - t0
+    emit(dict(config="C3-plan",
+              cpu_oracle_10k_subset_s=cpu_sub,
+              cpu_oracle_10k_subset_evals_per_s=o["model_evals"] / cpu_sub, workload="1 plan of 100,000 workloads, r_unit 0.01, b<=128 "
                                          "(grid-cooperative)",
               ms_per_plan=plan_ms, us_per_step=plan_ms * 1e3 / m, gpus=int(dp.gc[0].item()),
               reference_counters=st, candidate_evals_per_s=st["model_evals"] / (plan_ms / 1e3),
@@ -200,7 +213,14 @@ def c4():
     dp = DevicePlan(wl, hv, 32, rk, 0)
     ms = dp.time(3)
     st = dp.ref_stats()
-    emit(dict(config="C4", workload="4,096 scenarios x 1,000 workloads, 1 GPU (bench.py --gpus N shards)",
+    from oracle import oracle
+    threads = os.cpu_count() or 1
+    n_cpu = max(64, threads)
+    t0 = time.perf_counter()
+    oracle.plan_batch(wl[:n_cpu], hv, 32, rk, threads)
+    cpu_s = time.perf_counter() - t0
+    emit(dict(config="C4", cpu_oracle_plans_per_s=n_cpu / cpu_s, cpu_threads=threads,
+              cpu_sample=f"{n_cpu} scenarios on {threads} threads", workload="4,096 scenarios x 1,000 workloads, 1 GPU (bench.py --gpus N shards)",
               ms=ms, plans_per_s=4096 / (ms / 1e3), reference_counters=st,
               candidate_evals_per_s=st["model_evals"] / (ms / 1e3)))
 
@@ -226,7 +246,13 @@ def c5():
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     snap = sp.snapshot()
-    emit(dict(config="C5", workload=f"{S} independent streams x {L} arrivals = {S * L} arrivals, "
+    from oracle import oracle
+    from paper_2211_01713_b200.layout import hw_vector as _hv
+    t0 = time.perf_counter()
+    oracle.stream(wl[0], np.array(_hv(hw)), 32)
+    cpu_s = time.perf_counter() - t0
+    emit(dict(config="C5", cpu_oracle_arrivals_per_s_1core=L / cpu_s,
+              cpu_sample=f"one stream of {L} arrivals on 1 core", workload=f"{S} independent streams x {L} arrivals = {S * L} arrivals, "
                                     f"pushes of {chunk} arrivals per stream",
               ms=ms, arrivals_per_s=S * L / (ms / 1e3), us_per_push=ms * 1e3 / len(chunks),
               gpus_open=int(snap["gpu_count"].sum()),
