@@ -233,18 +233,27 @@ def c5():
     wl, _ = synth.scenarios(S, L, hw, seed=5)
     d_wl = torch.from_numpy(wl).to(dev)
     chunks = [d_wl[:, :, k:k + chunk].contiguous() for k in range(0, L, chunk)]
-    sp = StreamPlanner(hw, capacity=L, n_streams=S)
-    for c in chunks:  # warm-up pass
-        sp.push_device(c)
-    torch.cuda.synchronize()
-    sp.reset()
-    a, b = events()
-    a.record()
+    by_width = {}
+    for tag, fl in (("1 warp", 0), ("2 warps", 32), ("4 warps", 64)):
+        sp = StreamPlanner(hw, capacity=L, n_streams=S, flags=fl)
+        for c in chunks:  # warm-up pass
+            sp.push_device(c)
+        torch.cuda.synchronize()
+        sp.reset()
+        a, b = events()
+        a.record()
+        for c in chunks:
+            sp.push_device(c)
+        b.record()
+        torch.cuda.synchronize()
+        by_width[tag] = a.elapsed_time(b)
+        del sp
+        torch.cuda.empty_cache()
+    best = min(by_width, key=by_width.get)
+    ms = by_width[best]
+    sp = StreamPlanner(hw, capacity=L, n_streams=S, flags={"1 warp": 0, "2 warps": 32, "4 warps": 64}[best])
     for c in chunks:
         sp.push_device(c)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
     snap = sp.snapshot()
     from oracle import oracle
     from paper_2211_01713_b200.layout import hw_vector as _hv
@@ -255,6 +264,7 @@ def c5():
               cpu_sample=f"one stream of {L} arrivals on 1 core", workload=f"{S} independent streams x {L} arrivals = {S * L} arrivals, "
                                     f"pushes of {chunk} arrivals per stream",
               ms=ms, arrivals_per_s=S * L / (ms / 1e3), us_per_push=ms * 1e3 / len(chunks),
+              group_width=best, ms_by_group_width=by_width,
               gpus_open=int(snap["gpu_count"].sum()),
               rejected=int((snap["gpu_of"] < 0).sum()),
               multi_gpu="independent streams shard across ranks (SURVEY §8e option B)"))
