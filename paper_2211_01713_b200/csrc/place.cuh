@@ -676,6 +676,9 @@ k_place(PlanParams P) {
     const bool exact = (P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY);
     const bool margin = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
     // the newcomer (planner.py:291-292)
+#if IGP_TIMING
+    long long tm0 = clock64();
+#endif
     const double *ck = cold + (size_t)k * C_NF;
     const double *nk_rec = nwt + (size_t)k * R_NF;
     const int need = (int)ck[C_LB];
@@ -697,6 +700,9 @@ k_place(PlanParams P) {
     group_sync<GW>();
     unsigned long long my_best = NO_KEY;
     const int ncand = sE[need];  // candidates: the slack-order prefix with slack >= need
+#if IGP_TIMING
+    long long tm1 = clock64() + ncand * 0;
+#endif
 
     // ---- the step's candidates: per-lane state machine with dynamic refill ----
     // A lane owns at most one candidate GPU.  One loop iteration advances every
@@ -1091,6 +1097,9 @@ k_place(PlanParams P) {
     };
 
     run_step(false);
+#if IGP_TIMING
+    long long tm2 = clock64();
+#endif
     group_sync<GW>();
     if (t == 0 && !n_ready) mbar_wait(&nbar[grp], n_phase);  // retire this step's row copy
     n_ready = true;
@@ -1152,6 +1161,9 @@ k_place(PlanParams P) {
       committer = wi == 0;
     }
 
+#if IGP_TIMING
+    long long tm3 = clock64();
+#endif
     // ---- commit (planner.py:312-319), one warp of the group ----
     if (committer) {
       if (bk == NO_KEY) {
@@ -1360,6 +1372,15 @@ k_place(PlanParams P) {
         }
       }
     }
+#if IGP_TIMING
+    if (s == 0 && threadIdx.x == 0 && P.stats) {  // phase cycles of scenario 0, warp 0
+      long long tm4 = clock64();
+      atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S], (unsigned long long)(tm1 - tm0));
+      atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 1], (unsigned long long)(tm2 - tm1));
+      atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 2], (unsigned long long)(tm3 - tm2));
+      atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 3], (unsigned long long)(tm4 - tm3));
+    }
+#endif
     if (bk == NO_KEY) G += 1;
     sflags |= aflags;  // an admitted risky arrival can raise in later steps
     if (committer) fence_async_global();  // commit writes -> next step's tile copies
