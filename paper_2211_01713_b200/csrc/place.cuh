@@ -772,7 +772,15 @@ k_place(PlanParams P) {
         // warp-uniform stop (set by the serial replay's first raising candidate)
         if (__any_sync(FULL, stop)) break;
         const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
-        if (idle) {
+#ifndef IGP_REFILL_MIN
+#define IGP_REFILL_MIN 24
+#endif
+        // One-warp scenarios refill idle lanes in batches: the new candidates'
+        // tile copies then overlap, instead of each single refill exposing its
+        // own latency to the whole warp (24 of 32 measured best: +4.6%).  A
+        // warp with no busy lane always refills.
+        constexpr int refill_min = (GW == 1 && !COOP) ? IGP_REFILL_MIN : 1;
+        if (idle && (serial || __popc(idle) >= refill_min || idle == (FULL & take_mask))) {
           const int nidle = __popc(idle);
           if constexpr (COOP) {  // the other warps' results prune this warp's candidates
             if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[k & 1]));
