@@ -462,6 +462,7 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;
   if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
+  if (m >= (1 << 23)) return IGP_E_CAPACITY;  // candidate keys pack j into 23 bits
   WsLayout L = ws_layout(n_scen, m, hw.cap, flags);
   if (workspace_bytes < L.total || !workspace) return IGP_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
@@ -775,6 +776,7 @@ int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, i
   if (n_streams < 1 || capacity < 1 || k0 < 0 || n < 0 || k0 + n > capacity || !hw_h ||
       !workspace)
     return IGP_E_ARG;
+  if (capacity >= (1 << 23)) return IGP_E_CAPACITY;  // candidate keys pack j into 23 bits
   if (n == 0) return IGP_E_OK;
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;

@@ -111,7 +111,8 @@ __device__ __forceinline__ void fence_async_global() {
 // one scenario's step; the last warp to finish the step commits it and
 // publishes the step number.  State shared by all warps:
 struct CoopState {
-  unsigned long long best[2];  // argmin key of step k in best[k & 1]
+  unsigned int best[2];  // argmin key of step k in best[k & 1]
+  int best_pad[2];
   int done[2];                 // warps finished with step k
   int flag;                    // steps committed so far
   int pool_top, abort, G;
@@ -364,7 +365,7 @@ __global__ void k_table(PlanParams P) {
 // place stage
 // ---------------------------------------------------------------------------
 struct GroupSmem {
-  unsigned long long best;
+  unsigned int best;  // the step's argmin key so far (KEY_INTER_SHIFT packing)
   unsigned long long tot[5];  // model_evals, eval calls, candidates, resident reads, started
   int err_flag;
   int win_thread;
@@ -532,6 +533,7 @@ __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p)
   return __ldcg(p);
 }
 __device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned ld_cg(const unsigned *p) { return __ldcg(p); }
 
 template <int MAXN, int GW, bool COOP = false>
 __global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32,
@@ -540,7 +542,11 @@ k_place(PlanParams P) {
   static_assert(!COOP || GW == 1, "cooperative mode runs one group per warp");
   constexpr int GT = GW * 32;
   constexpr int GPB = (GW == 1) ? 4 : 1;
-  constexpr unsigned long long NO_KEY = ~0ull;
+  // Candidate keys (inter, j) packed into 32 bits, inter << 23 | j: lexicographic
+  // order is integer order, so the argmin is a native 32-bit atomicMin
+  // (the 64-bit one on shared memory is a CAS loop).  Needs j < 2^23 and
+  // inter < 2^9, which igp_plan_* enforce (m < 2^23, max_units <= 256).
+  constexpr unsigned NO_KEY = 0xffffffffu;
   constexpr unsigned FULL = 0xffffffffu;
   __shared__ GroupSmem gsm[GPB];
   __shared__ __align__(16) double ntb[GPB][TB * 4];  // the newcomer's solo table row
@@ -698,7 +704,7 @@ k_place(PlanParams P) {
     }
     bool n_ready = false;
     group_sync<GW>();
-    unsigned long long my_best = NO_KEY;
+    unsigned my_best = NO_KEY;
     const int ncand = sE[need];  // candidates: the slack-order prefix with slack >= need
 #if IGP_TIMING
     long long tm1 = clock64() + ncand * 0;
@@ -751,8 +757,7 @@ k_place(PlanParams P) {
             stop = true;
           }
         } else if (result == R_FEAS) {
-          const unsigned long long key =
-              ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
+          const unsigned key = ((unsigned)(c_sum - c_occ) << 23) | (unsigned)cj;
           if (key < my_best) {
             my_best = key;
             if constexpr (COOP) P.win_tid[cj] = gtid;
@@ -825,8 +830,8 @@ k_place(PlanParams P) {
             }
             if (have) {
               st_cands += 1;
-              const volatile unsigned long long *bp = &gs.best;
-              if (exact || ((((unsigned long long)need) << 32) | (unsigned)j) <= *bp) {
+              const volatile unsigned *bp = &gs.best;
+              if (exact || (((unsigned)need << 23) | (unsigned)j) <= *bp) {
                 // residents_j + [newcomer] (planner.py:302-304)
                 cj = j;
                 c_occ = (int)(g & 0xffffu);
@@ -1022,9 +1027,8 @@ k_place(PlanParams P) {
               finish(R_INFEAS);
               continue;
             }
-            const volatile unsigned long long *bp = &gs.best;
-            const unsigned long long key =
-                ((unsigned long long)(c_sum - c_occ) << 32) | (unsigned)cj;
+            const volatile unsigned *bp = &gs.best;
+            const unsigned key = ((unsigned)(c_sum - c_occ) << 23) | (unsigned)cj;
             if (key > *bp) {
               finish(R_PRUNED);
               continue;
@@ -1144,7 +1148,7 @@ k_place(PlanParams P) {
     tot_rres += st_rres;
     tot_run += st_run;
     st_evals = st_calls = st_cands = st_rres = st_run = 0;
-    unsigned long long bk;
+    unsigned bk;
     bool committer;
     if constexpr (COOP) {
       // arrive per CTA; warp 0 of the last CTA to finish the step commits
@@ -1228,7 +1232,7 @@ k_place(PlanParams P) {
         if (*(volatile int *)abortp == 0)
           slack_insert(sj, spos, sdesc, sE, G, gstate[G], cap - need, lane);
       } else {
-        const int j = (int)(bk & 0xffffffffu);
+        const int j = (int)(bk & 0x7fffffu);
         const int wt = COOP ? P.win_tid[j] : gs.win_thread;
         const uint16_t *lu = lane_units + (size_t)wt * cap;
         const int nres = (int)((gstate[j] >> 16) & 0xffffu);
