@@ -516,6 +516,8 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.err = err;
   if (stages & 1) {
     CK(cudaMemsetAsync(P.sflags, 0, (size_t)n_scen * 4, st));
+    // every byte of the error records (incl. padding) is defined for the caller
+    CK(cudaMemsetAsync(err, 0, (size_t)n_scen * sizeof(igp_error), st));
     k_fill_int<<<nblk(n_scen, 256), 256, 0, st>>>(P.perr, n_scen, INT_MAX);
     if (m > 0) {
       const long long tot = (long long)n_scen * m;
@@ -765,6 +767,8 @@ int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int
   StreamLayout X = stream_layout(n_streams, capacity, hw.cap, flags);
   if (workspace_bytes < X.total) return IGP_E_ARG;
   CK(cudaMemsetAsync((char *)workspace + X.sstate, 0, (size_t)n_streams * 16,
+                     (cudaStream_t)stream));
+  CK(cudaMemsetAsync((char *)workspace + X.err, 0, (size_t)n_streams * sizeof(igp_error),
                      (cudaStream_t)stream));
   return IGP_E_OK;
 }

@@ -464,8 +464,10 @@ __device__ __forceinline__ void slack_move_down(int32_t *sj, int32_t *spos,
       const int sb = a - i;
       q = sE[sb] - 1;
       dst = i == 0 ? p0 : sE[sb + 1] - 1;
-      xj = sj[q];
-      xd = sdesc[q];
+      if (q != dst) {  // an empty bucket makes the swap a no-op
+        xj = sj[q];
+        xd = sdesc[q];
+      }
     }
     __syncwarp();
     if (i < steps && q != dst) {
@@ -498,8 +500,10 @@ __device__ __forceinline__ void slack_insert(int32_t *sj, int32_t *spos,
     if (i < s) {
       u = sE[i + 1];
       dst = i == 0 ? j : sE[i];
-      xj = sj[u];
-      xd = sdesc[u];
+      if (u != dst) {  // an empty bucket makes the swap a no-op
+        xj = sj[u];
+        xd = sdesc[u];
+      }
     }
     __syncwarp();
     if (i < s && u != dst) {
