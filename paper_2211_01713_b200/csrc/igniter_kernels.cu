@@ -483,6 +483,7 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.sj = (int32_t *)(ws + L.sj);
   P.spos = (int32_t *)(ws + L.spos);
   P.sE = (int32_t *)(ws + L.sE);
+  P.nxt = (double *)(ws + L.nxt);
   P.wl = wl;
   P.rank = name_rank;
   P.rank_stride = rank_stride;
@@ -747,6 +748,7 @@ static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const 
   P.sj = (int32_t *)(ws + L.sj);
   P.spos = (int32_t *)(ws + L.spos);
   P.sE = (int32_t *)(ws + L.sE);
+  P.nxt = (double *)(ws + L.nxt);
   P.gpu_count = (int32_t *)(ws + X.gc);
   P.stats = nullptr;
   P.err = (igp_error *)(ws + X.err);

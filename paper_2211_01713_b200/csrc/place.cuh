@@ -34,8 +34,17 @@ constexpr int TILE0 = 4;   // initial tile capacity
 // pool record of one resident (96 B): its solo terms at the committed units,
 // t_sch for the next candidate size, the transfer / budget constants, and the
 // solo terms one unit up (a first bump inside a candidate needs no lookup)
+#ifndef IGP_SPLIT_NEXT
+#define IGP_SPLIT_NEXT 1
+#endif
+#if IGP_SPLIT_NEXT
+// 64-byte records; the next-unit solo terms live in a parallel pool array
+// (NEXT_AT) that the tile copy does not carry
+enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_NF };
+#else
 enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_KA1, R_PW1, R_CA1,
        R_ERR1, R_NF };
+#endif
 enum { SF_RISKY = 1, SF_NO_MARGIN = 2 };
 enum { R_FEAS = 0, R_INFEAS = 1, R_PRUNED = 2, R_ERROR = 3 };
 
@@ -49,7 +58,7 @@ struct Meta {
 // with one TMA bulk copy (records, meta, the GPU's Neumaier fold state);
 // residents beyond SLOT are read from the global pool.
 #ifndef IGP_SLOT
-#define IGP_SLOT 3
+#define IGP_SLOT 4
 #endif
 constexpr int SLOT = IGP_SLOT;
 static_assert(SLOT >= 1 && SLOT <= 4, "the tile header carries the first four residents' meta");
@@ -60,14 +69,18 @@ static_assert(SLOT >= 1 && SLOT <= 4, "the tile header carries the first four re
 struct __align__(16) TileHeader {
   double gf[4];  // Neumaier (s, c) of the power and cache sums over residents
   Meta meta[4];  // (workload, units, lower bound) of residents 0..3
+#if !IGP_SPLIT_NEXT
   double pad[4];
+#endif
 };
 static_assert(sizeof(TileHeader) == R_NF * 8, "the header occupies one record slot");
 
 struct __align__(16) LaneSlot {
   double gf[4];  // staged header ...
   Meta meta[4];
+#if !IGP_SPLIT_NEXT
   double hpad[4];
+#endif
   double rec[SLOT][R_NF];  // ... and the first SLOT resident records
   unsigned long long mbar;
   unsigned long long pad;
@@ -124,7 +137,7 @@ constexpr int COOP_MAX_LANES = 160 * 512;  // lane_units rows reserved for the c
 
 struct WsLayout {
   size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
-      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, total;
+      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, nxt, total;
   int lanes;
   int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
@@ -170,6 +183,7 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.sj = off; off = align_up(off + Sm * 4);
   L.spos = off; off = align_up(off + Sm * 4);
   L.sE = off; off = align_up(off + (size_t)S * (capx + 2) * 4);
+  L.nxt = off; off = align_up(off + (IGP_SPLIT_NEXT ? Sp * 32 : 32));
   L.total = off;
   return L;
 }
@@ -206,6 +220,7 @@ struct PlanParams {
   // per open GPU j: occupied units | residents << 16 | tile offset << 32
   unsigned long long *gstate;
   double *cold, *nw, *tbl, *gfold, *rec, *frec, *pfx;
+  double *nxt;  // IGP_SPLIT_NEXT: next-unit solo terms per pool record
   Meta *meta;
   uint16_t *lane_units;
   // outputs
@@ -624,6 +639,12 @@ k_place(PlanParams P) {
   double *gfold = P.gfold + sm * 4;
   const size_t sp = (size_t)s * (size_t)P.pool_recs;
   double *rec = P.rec + sp * R_NF;
+#if IGP_SPLIT_NEXT
+  double *nxt = P.nxt + sp * 4;
+#define NEXT_AT(ri) (nxt + (size_t)(ri) * 4)
+#else
+#define NEXT_AT(ri) (rec + (size_t)(ri) * R_NF + R_KA1)
+#endif
   double *frec = P.frec + sp * 2;
   double *pfx = P.pfx + sp * 4;
   Meta *meta = P.meta + sp;
@@ -1062,11 +1083,19 @@ k_place(PlanParams P) {
             const Meta mt = sl->meta[i];
             const int u = (int)mt.u + 1;
             if (!((c_sb >> i) & 1u)) {  // one unit above the committed units
+#if IGP_SPLIT_NEXT
+              const double *r = NEXT_AT(c_off + i);
+              so.ka = r[0];
+              so.pw = r[1];
+              so.ca = r[2];
+              so.err = (int)r[3];
+#else
               const double *r = sl->rec[i];
               so.ka = r[R_KA1];
               so.pw = r[R_PW1];
               so.ca = r[R_CA1];
               so.err = (int)r[R_ERR1];
+#endif
               c_sb |= 1u << i;
             } else {
               so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
@@ -1202,10 +1231,11 @@ k_place(PlanParams P) {
             r[R_PW] = nw_pw;
             {
               const Solo s1 = solo_lookup(tbl, cold, hw, k, need, need + 1);
-              r[R_KA1] = s1.ka;
-              r[R_PW1] = s1.pw;
-              r[R_CA1] = s1.ca;
-              r[R_ERR1] = (double)s1.err;
+              double *nx = NEXT_AT(off);
+              nx[0] = s1.ka;
+              nx[1] = s1.pw;
+              nx[2] = s1.ca;
+              nx[3] = (double)s1.err;
             }
             frec[(size_t)off * 2] = nw_pw;
             frec[(size_t)off * 2 + 1] = nw_ca;
@@ -1258,6 +1288,10 @@ k_place(PlanParams P) {
 #pragma unroll
               for (int f = 0; f < R_NF; ++f)
                 rec[(size_t)(noff + r) * R_NF + f] = rec[(size_t)(off + r) * R_NF + f];
+#if IGP_SPLIT_NEXT
+#pragma unroll
+              for (int f = 0; f < 4; ++f) NEXT_AT(noff + r)[f] = NEXT_AT(off + r)[f];
+#endif
               frec[(size_t)(noff + r) * 2] = frec[(size_t)(off + r) * 2];
               frec[(size_t)(noff + r) * 2 + 1] = frec[(size_t)(off + r) * 2 + 1];
               meta[noff + r] = meta[off + r];
@@ -1290,10 +1324,11 @@ k_place(PlanParams P) {
                 rr[R_KA] = so.ka;
                 rr[R_CA] = so.ca;
                 rr[R_PW] = so.pw;
-                rr[R_KA1] = s1.ka;
-                rr[R_PW1] = s1.pw;
-                rr[R_CA1] = s1.ca;
-                rr[R_ERR1] = (double)s1.err;
+                double *nx = NEXT_AT(off + r);
+                nx[0] = s1.ka;
+                nx[1] = s1.pw;
+                nx[2] = s1.ca;
+                nx[3] = (double)s1.err;
                 frec[(size_t)(off + r) * 2] = so.pw;
                 frec[(size_t)(off + r) * 2 + 1] = so.ca;
                 mt.u = (uint16_t)nu;
@@ -1313,10 +1348,11 @@ k_place(PlanParams P) {
               rr[R_KA] = so.ka;
               rr[R_CA] = so.ca;
               rr[R_PW] = so.pw;
-              rr[R_KA1] = s1.ka;
-              rr[R_PW1] = s1.pw;
-              rr[R_CA1] = s1.ca;
-              rr[R_ERR1] = (double)s1.err;
+              double *nx = NEXT_AT(off + r);
+              nx[0] = s1.ka;
+              nx[1] = s1.pw;
+              nx[2] = s1.ca;
+              nx[3] = (double)s1.err;
               rr[R_TSN] = (ksch + dnext) * nkern;
               rr[R_ACACHE] = nw_acache;
               rr[R_TLOAD] = nw_tload;
