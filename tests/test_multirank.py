@@ -75,3 +75,53 @@ def test_shard_bounds_cover_every_scenario_once():
                 a, b = shard.shard_bounds(n, r, w)
                 seen.extend(range(a, b))
             assert seen == list(range(n))
+
+
+def _stream_worker(rank, world, port, n_streams, length, out_path):
+    """Config 5 sharded as independent streams (SURVEY §8e option B): rank r
+    runs its block of streams in arrival order, then the per-arrival records
+    are all-gathered exactly like scenario plans."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+    from paper_2211_01713_b200 import synth
+    from paper_2211_01713_b200.layout import hw_vector
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from instances import make_v100
+    hw = make_v100()
+    wl, _ = synth.scenarios(n_streams, length, hw, seed=5)
+    hv = np.array(hw_vector(hw))
+    a, b = shard.shard_bounds(n_streams, rank, world)
+    runs = [oracle.stream(wl[s], hv, 32) for s in range(a, b)]
+    if runs:
+        local = torch.from_numpy(shard.pack_records(np.stack([r["gpu_of"] for r in runs]),
+                                                    np.stack([r["units"] for r in runs]),
+                                                    np.array([r["gpu_count"] for r in runs])))
+    else:
+        local = torch.zeros((0, shard.record_width(length)), dtype=torch.int32)
+    full = shard.gather_records(local, n_streams, world)
+    if rank == 0:
+        np.save(out_path, full.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_streams", [(2, 4), (3, 5)])
+def test_sharded_streams_gather_over_gloo(tmp_path, world, n_streams, oracle_lib):
+    length = 150
+    out = str(tmp_path / "streams.npy")
+    mp.start_processes(_stream_worker, args=(world, _free_port(), n_streams, length, out),
+                       nprocs=world, join=True, start_method="spawn")
+    gpu_of, units, gc = shard.unpack_records(np.load(out), length)
+    from paper_2211_01713_b200 import synth
+    from paper_2211_01713_b200.layout import hw_vector
+    from instances import make_v100
+    hw = make_v100()
+    wl, _ = synth.scenarios(n_streams, length, hw, seed=5)
+    for s in range(n_streams):
+        r = oracle_lib.stream(wl[s], np.array(hw_vector(hw)), 32)
+        np.testing.assert_array_equal(gpu_of[s], r["gpu_of"])
+        np.testing.assert_array_equal(units[s], r["units"])
+        assert gc[s] == r["gpu_count"]
