@@ -37,6 +37,10 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #ifndef IGP_SPLIT_NEXT
 #define IGP_SPLIT_NEXT 1
 #endif
+#ifndef IGP_PF_NEXT
+#define IGP_PF_NEXT 1  // L1 prefetch of the staged residents' next-unit terms
+#endif
+
 #if IGP_SPLIT_NEXT
 // 64-byte records; the next-unit solo terms live in a parallel pool array
 // (NEXT_AT) that the tile copy does not carry
@@ -871,6 +875,14 @@ k_place(PlanParams P) {
                   mbar_expect_tx(&sl->mbar, bytes);
                   bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, &sl->mbar);
                   c_wait = true;
+#if IGP_SPLIT_NEXT && IGP_PF_NEXT
+                  // the staged residents' next-unit terms, read on their first
+                  // bump (+1% at the headline; prefetching the residents beyond
+                  // the slot or the next newcomer measured within noise)
+                  asm volatile("prefetch.global.L1 [%0];" ::"l"(NEXT_AT(c_off)));
+                  asm volatile("prefetch.global.L1 [%0];" ::"l"(NEXT_AT(c_off + nst - 1)));
+#endif
+
                 }
                 c_sum = c_occ + need;
                 c_i = 0;
