@@ -544,6 +544,11 @@ __device__ __forceinline__ void slack_insert(int32_t *sj, int32_t *spos,
   __syncwarp();
 }
 
+template <bool B>
+struct BoolC {
+  static constexpr bool value = B;
+};
+
 template <int MAXN>
 struct LaneArrays {  // values of residents bumped inside the current candidate
   int u[MAXN];
@@ -748,7 +753,11 @@ k_place(PlanParams P) {
     // keys prune later candidates and lanes never wait for a round's longest
     // candidate.  serial != 0 replays the step in the reference's order on
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
-    auto run_step = [&](const bool serial) {
+    // serial and exact are compile-time per instantiation, so the common
+    // pruned step carries none of the exact-mode bookkeeping
+    auto run_step = [&](auto serial_c, auto exact_c) {
+      constexpr bool serial = decltype(serial_c)::value;
+      constexpr bool exact = decltype(exact_c)::value;
       int qhead = 0;
       int scan = 0;  // serial replay: next GPU index to test
       // cooperative mode: this lane's next candidate position; consecutive
@@ -1153,7 +1162,8 @@ k_place(PlanParams P) {
       }
     };
 
-    run_step(false);
+    if (exact) run_step(BoolC<false>{}, BoolC<true>{});
+    else run_step(BoolC<false>{}, BoolC<false>{});
 #if IGP_TIMING
     long long tm2 = clock64();
 #endif
@@ -1166,7 +1176,7 @@ k_place(PlanParams P) {
       // exact mode only: replay the step in the reference's candidate order to
       // find the first raising candidate and the PlanStats at that point
       st_evals = st_calls = st_cands = st_rres = st_run = 0;
-      if (wi == 0) run_step(true);
+      if (wi == 0) run_step(BoolC<true>{}, BoolC<true>{});
       if (t != 0) st_evals = st_calls = st_cands = st_rres = st_run = 0;
       tot_evals += st_evals;
       tot_calls += st_calls;
