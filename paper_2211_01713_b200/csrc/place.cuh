@@ -680,7 +680,9 @@ k_place(PlanParams P) {
     for (int x = t; x < cap + 2; x += GT) sE[x] = 0;
   }
   long long tot_evals = 0, tot_calls = 0, tot_cands = 0, tot_rres = 0, tot_run = 0;
-  long long st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
+  // per-step counters (one lane's share); only exact steps keep the
+  // PlanStats-only ones
+  int st_evals = 0, st_calls = 0, st_cands = 0, st_rres = 0, st_run = 0;
   int fail_code = 0;
   ErrOut eo_fail;
   eo_fail.code = 0;
@@ -816,12 +818,13 @@ k_place(PlanParams P) {
         if (__any_sync(FULL, stop)) break;
         const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
 #ifndef IGP_REFILL_MIN
-#define IGP_REFILL_MIN 24
+#define IGP_REFILL_MIN 28
 #endif
         // One-warp scenarios refill idle lanes in batches: the new candidates'
         // tile copies then overlap, instead of each single refill exposing its
-        // own latency to the whole warp (24 of 32 measured best: +4.6%).  A
-        // warp with no busy lane always refills.
+        // own latency to the whole warp (+4.6% at 24 of 32 over single
+        // refills; 28 a further +0.6%, 20 -0.6%).  A warp with no busy lane
+        // always refills.
         constexpr int refill_min = (GW == 1 && !COOP) ? IGP_REFILL_MIN : 1;
         if (idle && (serial || __popc(idle) >= refill_min || idle == (FULL & take_mask))) {
           const int nidle = __popc(idle);
@@ -867,7 +870,7 @@ k_place(PlanParams P) {
               }
             }
             if (have) {
-              st_cands += 1;
+              if (exact) st_cands += 1;
               const volatile unsigned *bp = &gs.best;
               if (exact || (((unsigned)need << 23) | (unsigned)j) <= *bp) {
                 // residents_j + [newcomer] (planner.py:302-304)
@@ -875,7 +878,7 @@ k_place(PlanParams P) {
                 c_occ = (int)(g & 0xffffu);
                 c_nres = (int)((g >> 16) & 0xffffu);
                 c_off = (int)(g >> 32);
-                st_rres += c_nres;
+                if (exact) st_rres += c_nres;
                 st_run += 1;
                 {  // stage the tile header and the first SLOT records: one bulk copy
                   const int nst = c_nres < SLOT ? c_nres : SLOT;
@@ -998,7 +1001,7 @@ k_place(PlanParams P) {
           c_f = f;
           c_one = f == hw.fmax && hw.margin_ok;
           c_inv = c_one ? 1.0 : hw.fmax / f;
-          st_evals += c_nres + 1;
+          if (exact) st_evals += c_nres + 1;
           st_calls += 1;
           c_need = false;
         }
