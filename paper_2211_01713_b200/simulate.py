@@ -46,6 +46,14 @@ class SimConfig:
 
 
 @dataclass(frozen=True)
+class RequestRecord:
+    workload: str
+    arrival_ms: float
+    dispatch_ms: float
+    complete_ms: float
+
+
+@dataclass(frozen=True)
 class WorkloadReport:
     workload: str
     offered_rps: float
@@ -68,8 +76,10 @@ class SimReport:
         return [w.workload for w in self.workloads if w.violation]
 
 
-def replay_arrays(rate_rps, batch, service_ms, cfg: SimConfig, device=None):
-    """Device replay of n workloads; numpy arrays in, dict of numpy arrays out."""
+def replay_arrays(rate_rps, batch, service_ms, cfg: SimConfig, device=None, *, starts=False):
+    """Device replay of n workloads; numpy arrays in, dict of numpy arrays out.
+    With starts=True the result also holds every batch's start time
+    (``starts``, workload w's batches from ``seg[w]``)."""
     torch = _device._torch()
     lib = _native.lib_for_compute()
     device = _device._dev(device)
@@ -96,14 +106,53 @@ def replay_arrays(rate_rps, batch, service_ms, cfg: SimConfig, device=None):
         _device._check(rc)
         oi = i32.cpu().numpy()[:, :n]
         of = f64.cpu().numpy()[:, :n]
-    return dict(max_depth=oi[0], backlog=oi[1], completed=oi[2], p50=of[0], p99=of[1],
-                achieved=of[2])
+        out = dict(max_depth=oi[0], backlog=oi[1], completed=oi[2], p50=of[0], p99=of[1],
+                   achieved=of[2])
+        if starts:
+            out.update(starts=scratch[1].cpu().numpy(), seg=seg)
+    return out
+
+
+def arrival_count(rate_rps: float, duration_ms: float) -> int:
+    """Number of constant-rate arrivals t_k = k * (1000 / rate) < duration
+    (``_arrival_times``, simulate.py:79-85), without the loop."""
+    if not duration_ms > 0.0:
+        return 0
+    spacing = 1000.0 / rate_rps
+    k = max(1, math.ceil(duration_ms / spacing))
+    while k * spacing < duration_ms:
+        k += 1
+    while k > 1 and (k - 1) * spacing >= duration_ms:
+        k -= 1
+    return k
+
+
+def _workload_trace(name, rate_rps, batch, service_ms, starts, cfg):
+    """The RequestRecords of one workload in the reference's order
+    (simulate.py:118-124): batch after batch, members in arrival order."""
+    spacing = 1000.0 / rate_rps
+    out = []
+    for q in range(arrival_count(rate_rps, cfg.duration_ms) // batch):
+        start = float(starts[q])
+        done = start + service_ms
+        out.extend(RequestRecord(name, r * spacing if r else 0.0, start, done)
+                   for r in range(q * batch, (q + 1) * batch))
+    return out
+
+
+def write_trace_csv(path, trace) -> None:
+    """Per-request trace: workload,arrival_ms,dispatch_ms,complete_ms (simulate.py:201-209)."""
+    with open(path, "w") as handle:
+        handle.write("workload,arrival_ms,dispatch_ms,complete_ms\n")
+        for r in trace:
+            handle.write(f"{r.workload},{r.arrival_ms!r},{r.dispatch_ms!r},{r.complete_ms!r}\n")
 
 
 def simulate(plan, specs: Mapping, coefs: Mapping, hw, cfg: SimConfig, *, collect_trace: bool = False):
-    """Replay every workload of a plan; interference is frozen at plan time."""
-    if collect_trace:
-        raise NotImplementedError("per-request traces are not materialised by the device replay")
+    """Replay every workload of a plan; interference is frozen at plan time.
+    With collect_trace=True returns (report, trace) like the reference
+    (simulate.py:192-198); the trace is rebuilt from the device's batch start
+    times (arrival k at k * spacing, completion at start + t_inf)."""
     items = []  # (name, batch, service t_inf)
     for gpu in plan.gpus:
         predicted = predict_gpu(gpu.allocations, specs, coefs, hw)
@@ -113,8 +162,9 @@ def simulate(plan, specs: Mapping, coefs: Mapping, hw, cfg: SimConfig, *, collec
     if cfg.arrival == "poisson" and items:
         random.Random((cfg.seed, 0))  # the reference's seed: TypeError on CPython >= 3.11
     r = replay_arrays([specs[n].rate_rps for n, _, _ in items], [b for _, b, _ in items],
-                      [s for _, _, s in items], cfg)
+                      [s for _, _, s in items], cfg, starts=collect_trace)
     reports = []
+    trace = []
     for i, (name, batch, _) in enumerate(items):
         if int(r["backlog"][i]) > UNSTABLE_QUEUE_FACTOR * batch:
             raise UnstableQueueError(name, int(r["backlog"][i]), UNSTABLE_QUEUE_FACTOR * batch)
@@ -124,4 +174,10 @@ def simulate(plan, specs: Mapping, coefs: Mapping, hw, cfg: SimConfig, *, collec
             workload=name, offered_rps=specs[name].rate_rps, achieved_rps=float(r["achieved"][i]),
             p50_ms=float(r["p50"][i]), p99_ms=p99, max_queue_depth=int(r["max_depth"][i]),
             completed=done, violation=bool(done) and p99 > specs[name].slo_ms))
-    return SimReport(cfg.duration_ms, cfg.warmup_ms, reports)
+        if collect_trace:
+            trace.extend(_workload_trace(name, specs[name].rate_rps, batch, items[i][2],
+                                         r["starts"][r["seg"][i]:], cfg))
+    report = SimReport(cfg.duration_ms, cfg.warmup_ms, reports)
+    if collect_trace:
+        return report, trace
+    return report

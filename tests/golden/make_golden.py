@@ -419,6 +419,23 @@ def simulate_case(workloads, hw, cfg, plan=None):
     return out
 
 
+def trace_case(workloads, hw, cfg):
+    """simulate(..., collect_trace=True): the per-request records
+    (simulate.py:192-197), as workload index + fp64 arrays."""
+    import importlib
+    gsim = importlib.import_module("gpuplanner.simulate")
+    out = simulate_case(workloads, hw, cfg)
+    specs = {s.name: s for s, _ in workloads}
+    coefs = {s.name: c for s, c in workloads}
+    _, trace = gsim.simulate(gp.plan(workloads, hw), specs, coefs, hw, cfg, collect_trace=True)
+    index = {str(n): i for i, n in enumerate(out["sim_names"])}
+    out.update(trace_w=np.array([index[r.workload] for r in trace], np.int32),
+               trace_arrival=np.array([r.arrival_ms for r in trace]),
+               trace_dispatch=np.array([r.dispatch_ms for r in trace]),
+               trace_complete=np.array([r.complete_ms for r in trace]))
+    return out
+
+
 def stream_case(workloads, hw, b_max=32):
     out = pack_instance(workloads, hw, b_max)
     gpu_of, pos, code, units = stream_reference(workloads, hw, b_max)
@@ -609,6 +626,16 @@ def main():
              "UnstableQueueError: batch 1 at 2.5% of a device cannot keep up")
         save("sim_poisson", simulate_case(twelve[:3], v100, gsim.SimConfig(1_000.0, arrival="poisson")),
              "poisson arrivals: the reference's tuple seed raises TypeError on CPython 3.12")
+
+    if "simtrace" in groups:
+        import importlib
+        gsim = importlib.import_module("gpuplanner.simulate")
+        twelve = support.twelve_workload_instance()
+        save("simtrace_c1_allwarm", trace_case(twelve[:5], v100, gsim.SimConfig(500.0, 500.0)),
+             "simulate(..., collect_trace=True), warmup == duration")
+        inst = support.random_instance(np.random.default_rng(90), 60, v100)
+        save("simtrace_rand60", trace_case(inst, v100, gsim.SimConfig(200.0, 50.0)),
+             "simulate(..., collect_trace=True), 60 workloads, 200 ms")
 
     # ---- component cases ------------------------------------------------
     if "component" not in groups:

@@ -69,3 +69,28 @@ def test_simulate_errors_like_reference():
         simulate(igp.plan(wls, hw), {s.name: s for s, _ in wls}, {s.name: c for s, c in wls}, hw,
                  _cfg(d))
     assert str(ei.value) == str(d["err_msg"])
+
+
+@pytest.mark.parametrize("case", G.names("simtrace_"))
+def test_trace_matches_reference(case, tmp_path):
+    from paper_2211_01713_b200.simulate import write_trace_csv
+    d = G.load(case)
+    wls = workloads_from_golden(d)
+    hw = hw_from_golden(d)
+    specs = {s.name: s for s, _ in wls}
+    coefs = {s.name: c for s, c in wls}
+    rep, trace = simulate(igp.plan(wls, hw), specs, coefs, hw, _cfg(d), collect_trace=True)
+    names = [str(x) for x in d["sim_names"]]
+    assert [r.workload for r in trace] == [names[i] for i in d["trace_w"]]
+    for key, attr in (("trace_arrival", "arrival_ms"), ("trace_dispatch", "dispatch_ms"),
+                      ("trace_complete", "complete_ms")):
+        np.testing.assert_array_equal(G.bits([getattr(r, attr) for r in trace]), G.bits(d[key]))
+    np.testing.assert_array_equal(G.bits([w.p99_ms for w in rep.workloads]), G.bits(d["p99"]))
+    path = tmp_path / "trace.csv"
+    write_trace_csv(path, trace)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "workload,arrival_ms,dispatch_ms,complete_ms"
+    assert len(lines) == len(trace) + 1
+    i = len(trace) // 2
+    assert lines[1 + i] == (f"{names[d['trace_w'][i]]},{float(d['trace_arrival'][i])!r},"
+                            f"{float(d['trace_dispatch'][i])!r},{float(d['trace_complete'][i])!r}")
