@@ -29,6 +29,10 @@
  *   igp_solo_grid_device
  *       replaces _Search.best_group_alloc oracle.py:77-114 for one-workload
  *                                  groups over every batch (the solo grid)
+ *   igp_components_device, igp_power_demand_device
+ *       replace the model's scalar component functions model.py:159-236
+ *                                  (transfer_latencies .. gpu_frequency,
+ *                                  power_demand), batched
  *   igp_prologue_device
  *       replaces appropriate_batch planner.py:76-92 and _lower_bound_units
  *                                  planner.py:95-120 (lower_bound_resources
@@ -260,6 +264,35 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
 int igp_group_search_device(const double *wl, int n, const int32_t *batch, const double *hw,
                             const int32_t *grid, int n_grid, unsigned long long *best,
                             int32_t *err, void *stream);
+
+/*
+ * The latency model's component functions (model.py:159-236), one query per
+ * index i, with the reference's operation order (bit-identical results).
+ *   wl       [IGP_WL_NF][n] fp64 query fields (field-major; only d_load,
+ *            d_feedback and the WorkloadCoefficients fields are read)
+ *   batch    [n] int32, r [n] resource fraction, co_cache [n] co-runners'
+ *            summed cache utilisation, n_col [n] co-located workloads,
+ *            p_dem [n] device power demand (W)
+ *   out      [n][10] fp64: t_load, t_feedback (transfer_latencies), r + k4,
+ *            solo_active_time, solo_power, solo_cache_util,
+ *            sched_delay_increase, sched_delay, active_time_with_interference,
+ *            gpu_frequency
+ *   code     [n] int32: 0, IGP_E_DENOM (r + k4 <= 0: solo_active_time and
+ *            everything built on it raise) or IGP_E_ACTIVE_TIME (k_act <= 0:
+ *            solo_power / solo_cache_util raise, model.py:178-183)
+ * All pointers are device pointers except hw (host, IGP_HW_* order).
+ */
+int igp_components_device(int n, const double *wl, const int32_t *batch, const double *r,
+                          const double *co_cache, const int32_t *n_col, const double *p_dem,
+                          const double *hw, double *out, int32_t *code, void *stream);
+
+/*
+ * power_demand (model.py:226-228): hw.power_idle_w + the CPython 3.12 sum
+ * (Neumaier-compensated, in order) of n solo powers; *out (device) = the
+ * idle draw when n == 0.
+ */
+int igp_power_demand_device(int n, const double *powers, const double *hw, double *out,
+                            void *stream);
 
 /*
  * Request-level replay of a plan (simulate._run_workload simulate.py:98-136

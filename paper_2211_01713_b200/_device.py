@@ -206,6 +206,41 @@ def eval_states(wl, batch, r, ptr, hw_vec, check_capacity=False, device=None):
     return rows, err
 
 
+def components(wl, batch, r, co_cache, n_col, p_dem, hw_vec, device=None):
+    """The model's component functions for n queries (igp_components_device):
+    ([n, 10] fp64 columns, [n] int32 error codes)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    wl = np.ascontiguousarray(wl, np.float64)
+    n = wl.shape[1]
+    h = hw_array(hw_vec)
+    with torch.cuda.device(device):
+        d = [_to_dev(np.ascontiguousarray(a, t), device) for a, t in (
+            (wl, np.float64), (batch, np.int32), (r, np.float64), (co_cache, np.float64),
+            (n_col, np.int32), (p_dem, np.float64))]
+        d_out = torch.empty((max(n, 1), 10), dtype=torch.float64, device=device)
+        d_code = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+        rc = lib.igp_components_device(n, *[_ptr(x) for x in d], _np_ptr(h), _ptr(d_out),
+                                       _ptr(d_code), _stream(device))
+        _check(rc)
+        return d_out.cpu().numpy()[:n], d_code.cpu().numpy()[:n]
+
+
+def power_demand(powers, hw_vec, device=None) -> float:
+    """hw idle draw + the CPython sum of the solo powers (igp_power_demand_device)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    device = _dev(device)
+    p = np.ascontiguousarray(powers, np.float64)
+    with torch.cuda.device(device):
+        d_p = _to_dev(p if len(p) else np.zeros(1), device)
+        d_out = torch.empty(1, dtype=torch.float64, device=device)
+        _check(lib.igp_power_demand_device(len(p), _ptr(d_p), _np_ptr(hw_array(hw_vec)),
+                                           _ptr(d_out), _stream(device)))
+        return float(d_out.cpu()[0])
+
+
 def alloc_units(wl, batch, r, ptr, hw_vec, device=None):
     """Batched Alg. 2 (reference evaluation sequence)."""
     torch = _torch()

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("IGP_LIB") or os.path.join(LIB_DIR, "libigniter_b200.s
 SOURCES = [os.path.join(PKG, "csrc", "igniter_kernels.cu")]
 DEPS = SOURCES + [os.path.join(PKG, "csrc", "exact_fp64.cuh"), os.path.join(PKG, "csrc", "place.cuh"),
                   os.path.join(PKG, "csrc", "grid.cuh"), os.path.join(PKG, "csrc", "exhaustive.cuh"),
-                  os.path.join(PKG, "csrc", "simulate.cuh"),
+                  os.path.join(PKG, "csrc", "simulate.cuh"), os.path.join(PKG, "csrc", "components.cuh"),
                   os.path.join(REPO, "include", "igniter_b200.h")]
 
 NVCC_FLAGS = [
@@ -96,6 +96,8 @@ PROTOTYPES = {
     "igp_group_search_device": (_I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _VP, _VP]),
     "igp_simulate_device": (_I, [_I, _VP, _VP, _VP, ctypes.c_double, ctypes.c_double, _VP, _VP,
                                  _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "igp_components_device": (_I, [_I, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "igp_power_demand_device": (_I, [_I, _VP, _VP, _VP, _VP]),
     "igp_stream_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I]),
     "igp_stream_reset_device": (_I, [_I, _I, _VP, _I, _VP, _SZ, _I, _VP]),
     "igp_stream_push_device": (_I, [_VP, _I, _I, _I, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP, _VP,

@@ -140,6 +140,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 #endif
 #include "exhaustive.cuh"
 #include "simulate.cuh"
+#include "components.cuh"
 
 namespace igp {
 
@@ -961,6 +962,36 @@ int igp_solo_grid_device(const double *wl, int m, const double *hw_h, int b_max,
   if (n_evals) CK(cudaMemsetAsync(n_evals, 0, sizeof(unsigned long long), st));
   k_solo_grid<<<nblk((long long)m * b_max, 256), 256, 0, st>>>(G);
   if (best_u && best_b) k_grid_best<<<nblk((long long)m * 32, 256), 256, 0, st>>>(G);
+  CK(cudaGetLastError());
+  return IGP_E_OK;
+}
+
+int igp_components_device(int n, const double *wl, const int32_t *batch, const double *r,
+                          const double *co_cache, const int32_t *n_col, const double *p_dem,
+                          const double *hw_h, double *out, int32_t *code, void *stream) {
+  if (n < 0 || !hw_h) return IGP_E_ARG;
+  if (n == 0) return IGP_E_OK;
+  if (!wl || !batch || !r || !co_cache || !n_col || !p_dem || !out || !code) return IGP_E_ARG;
+  CompParams C;
+  C.n = n;
+  C.hw = make_hw(hw_h, 1);
+  C.wl = wl;
+  C.batch = batch;
+  C.r = r;
+  C.co_cache = co_cache;
+  C.n_col = n_col;
+  C.p_dem = p_dem;
+  C.out = out;
+  C.code = code;
+  k_components<<<nblk(n, 128), 128, 0, (cudaStream_t)stream>>>(C);
+  CK(cudaGetLastError());
+  return IGP_E_OK;
+}
+
+int igp_power_demand_device(int n, const double *powers, const double *hw_h, double *out,
+                            void *stream) {
+  if (n < 0 || !hw_h || !out || (n > 0 && !powers)) return IGP_E_ARG;
+  k_power_demand<<<1, 32, 0, (cudaStream_t)stream>>>(n, powers, make_hw(hw_h, 1), out);
   CK(cudaGetLastError());
   return IGP_E_OK;
 }

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _device
 from .errors import native_exception
-from .layout import WL_NF, hw_vector, spec_coef_row
+from .layout import E_ACTIVE_TIME, E_DENOM, WL_NF, hw_vector, spec_coef_row
 
 
 @dataclass(frozen=True)
@@ -154,6 +154,104 @@ def slo_check(breakdown: LatencyBreakdown, spec: WorkloadSpec) -> SloCheck:
         latency_ok=bool(breakdown.t_inf_ms <= spec.slo_ms / 2.0),
         throughput_ok=bool(breakdown.throughput_rps >= spec.rate_rps),
     )
+
+
+# ---- component functions (model.py:159-236), evaluated on the device --------
+# Each call is one igp_components_device launch over a single query; the
+# columns follow include/igniter_b200.h.
+_K_TLOAD, _K_TFB, _K_DENOM, _K_KACT, _K_POWER, _K_CACHE, _K_SCHINC, _K_SCHED, _K_ACTINT, \
+    _K_FREQ = range(10)
+
+
+def _component(hw, *, spec=None, coef=None, batch=1, r=1.0, co_cache=0.0, n_col=1, p_dem=0.0):
+    row = np.zeros((WL_NF, 1))
+    if coef is not None:
+        row[:, 0] = spec_coef_row(spec, coef) if spec is not None else \
+            spec_coef_row(_ZeroSpec, coef)
+    elif spec is not None:
+        row[:, 0] = spec_coef_row(spec, _UnitCoef)
+    out, code = _device.components(row, [batch], [r], [co_cache], [n_col], [p_dem],
+                                   hw_vector(hw))
+    return out[0], int(code[0])
+
+
+class _ZeroSpec:  # spec fields a coefficient-only query does not read
+    slo_ms = rate_rps = d_load_mb = d_feedback_mb = 0.0
+
+
+class _NEUTRAL_HW:  # hardware fields the hardware-independent columns do not read
+    power_max_w = freq_max_mhz = pcie_bw_mb_per_ms = r_max = price_per_hour = f_min_frac = 1.0
+    power_idle_w = alpha_f = alpha_sch_ms = beta_sch_ms = 0.0
+    r_unit = 0.025
+
+
+class _UnitCoef:  # coefficient fields a spec-only query does not read
+    n_kernels = 1
+    k_sch_ms = k1 = k2 = k3 = k5 = alpha_power_w = beta_power_w = 0.0
+    alpha_cacheutil = beta_cacheutil = alpha_cache = 0.0
+    k4 = 1.0
+
+
+def _solo(coef, batch, r, need_positive):
+    out, code = _component(_NEUTRAL_HW, coef=coef, batch=batch, r=r)
+    if code == E_DENOM:
+        raise native_exception(code, float(out[_K_DENOM]), float(r), float(coef.k4))
+    if need_positive and code == E_ACTIVE_TIME:
+        raise native_exception(code, float(out[_K_KACT]), batch, float(r))
+    return out
+
+
+def transfer_latencies(spec: WorkloadSpec, batch: int, hw: HardwareProfile) -> tuple[float, float]:
+    """PCIe load/feedback latency of one batch, in ms (model.py:159-165)."""
+    out, _ = _component(hw, spec=spec, batch=batch)
+    return float(out[_K_TLOAD]), float(out[_K_TFB])
+
+
+def solo_active_time(coef: WorkloadCoefficients, batch: int, r: float) -> float:
+    """GPU active time (ms) of a batch running alone (model.py:168-175)."""
+    return float(_solo(coef, batch, r, False)[_K_KACT])
+
+
+def solo_power(coef: WorkloadCoefficients, batch: int, r: float) -> float:
+    """Solo power draw (W), linear in batch / k_act (model.py:186-190)."""
+    return float(_solo(coef, batch, r, True)[_K_POWER])
+
+
+def solo_cache_util(coef: WorkloadCoefficients, batch: int, r: float) -> float:
+    """Solo L2-cache utilisation clamped to [0, 1] (model.py:193-198)."""
+    return float(_solo(coef, batch, r, True)[_K_CACHE])
+
+
+def sched_delay_increase(hw: HardwareProfile, n_colocated: int) -> float:
+    """Per-kernel scheduling-delay increase (ms) from co-location (model.py:201-209)."""
+    out, _ = _component(hw, n_col=n_colocated)
+    return float(out[_K_SCHINC])
+
+
+def sched_delay(coef: WorkloadCoefficients, hw: HardwareProfile, n_colocated: int) -> float:
+    """Total kernel scheduling delay (ms) for one batch (model.py:212-216)."""
+    out, _ = _component(hw, coef=coef, n_col=n_colocated)
+    return float(out[_K_SCHED])
+
+
+def active_time_with_interference(coef: WorkloadCoefficients, batch: int, r: float,
+                                  co_cache_sum: float) -> float:
+    """Active time (ms) inflated by co-runners' summed cache use (model.py:219-223)."""
+    out, code = _component(_NEUTRAL_HW, coef=coef, batch=batch, r=r, co_cache=co_cache_sum)
+    if code == E_DENOM:
+        raise native_exception(code, float(out[_K_DENOM]), float(r), float(coef.k4))
+    return float(out[_K_ACTINT])
+
+
+def power_demand(hw: HardwareProfile, solo_powers) -> float:
+    """Device power demand (W): idle draw + the residents' solo power (model.py:226-228)."""
+    return _device.power_demand([float(p) for p in solo_powers], hw_vector(hw))
+
+
+def gpu_frequency(hw: HardwareProfile, p_demand: float) -> float:
+    """Operating frequency (MHz) under the power cap (model.py:231-236)."""
+    out, _ = _component(hw, p_dem=p_demand)
+    return float(out[_K_FREQ])
 
 
 class _Entry:

@@ -20,6 +20,7 @@ from 3.12 on and the reference depends on it (SURVEY.md finding 1).
 
 from __future__ import annotations
 
+import dataclasses
 import json
 import math
 import os
@@ -436,6 +437,65 @@ def trace_case(workloads, hw, cfg):
     return out
 
 
+def modelfn_case(seed, n, hw):
+    """The model's component functions (model.py:159-236) on n random queries,
+    including r + k4 <= 0 and k_act <= 0 rows; '' / message per function."""
+    from gpuplanner import model as gm
+    rng = np.random.default_rng(seed)
+    wls, batch, r, co, ncol, pdem = [], [], [], [], [], []
+    for i in range(n):
+        c = support.random_coefficients(rng)
+        kind = i % 10
+        if kind == 8:  # r + k4 <= 0
+            c = dataclasses.replace(c, k4=-float(rng.uniform(0.3, 1.2)))
+        elif kind == 9:  # k_act <= 0
+            c = dataclasses.replace(c, k5=-float(rng.uniform(50.0, 500.0)))
+        sp = gp.WorkloadSpec(f"q{i}", float(rng.uniform(20, 100)), float(rng.uniform(50, 6000)),
+                             float(rng.uniform(0.05, 1.0)), float(rng.uniform(0.001, 0.05)))
+        wls.append((sp, c))
+        batch.append(int(rng.integers(1, 129)))
+        r.append(float(rng.integers(1, 41)) * hw.r_unit)
+        co.append(float(rng.uniform(0.0, 3.0)))
+        ncol.append(int(rng.integers(0, 12)))
+        pdem.append(float(rng.uniform(0.5, 2.5)) * hw.power_max_w)
+    out = pack_instance(wls, hw, 128)
+
+    def run(fn):
+        vals, msgs = [], []
+        for i, (sp, c) in enumerate(wls):
+            try:
+                vals.append(float(fn(i, sp, c)))
+                msgs.append("")
+            except Exception as exc:  # noqa: BLE001 - recorded for the parity test
+                vals.append(float("nan"))
+                msgs.append(f"{type(exc).__name__}: {exc}")
+        return np.array(vals), np.array(msgs)
+
+    cols = {
+        "t_load": lambda i, sp, c: gm.transfer_latencies(sp, batch[i], hw)[0],
+        "t_fb": lambda i, sp, c: gm.transfer_latencies(sp, batch[i], hw)[1],
+        "k_act": lambda i, sp, c: gm.solo_active_time(c, batch[i], r[i]),
+        "power": lambda i, sp, c: gm.solo_power(c, batch[i], r[i]),
+        "cache": lambda i, sp, c: gm.solo_cache_util(c, batch[i], r[i]),
+        "sch_inc": lambda i, sp, c: gm.sched_delay_increase(hw, ncol[i]),
+        "sched": lambda i, sp, c: gm.sched_delay(c, hw, ncol[i]),
+        "act_int": lambda i, sp, c: gm.active_time_with_interference(c, batch[i], r[i], co[i]),
+        "freq": lambda i, sp, c: gm.gpu_frequency(hw, pdem[i]),
+    }
+    for k, fn in cols.items():
+        v, m = run(fn)
+        out[f"fn_{k}"] = v
+        out[f"msg_{k}"] = m
+    lists = [[float(x) for x in rng.uniform(10.0, 150.0, int(rng.integers(0, 14)))] for _ in range(64)]
+    lists[1] = [1e16, 1.0, -1e16, 3.5]  # compensation matters
+    out.update(q_batch=np.array(batch, np.int32), q_r=np.array(r), q_co=np.array(co),
+               q_ncol=np.array(ncol, np.int32), q_pdem=np.array(pdem),
+               pd_ptr=np.cumsum([0] + [len(x) for x in lists]).astype(np.int64),
+               pd_vals=np.array([x for xs in lists for x in xs]),
+               pd_out=np.array([gm.power_demand(hw, xs) for xs in lists]))
+    return out
+
+
 def stream_case(workloads, hw, b_max=32):
     out = pack_instance(workloads, hw, b_max)
     gpu_of, pos, code, units = stream_reference(workloads, hw, b_max)
@@ -626,6 +686,11 @@ def main():
              "UnstableQueueError: batch 1 at 2.5% of a device cannot keep up")
         save("sim_poisson", simulate_case(twelve[:3], v100, gsim.SimConfig(1_000.0, arrival="poisson")),
              "poisson arrivals: the reference's tuple seed raises TypeError on CPython 3.12")
+
+    if "modelfn" in groups:
+        save("modelfn_v100", modelfn_case(11, 1000, v100), "model.py:159-236 component functions")
+        save("modelfn_r01", modelfn_case(12, 500, support.make_v100(r_unit=0.01)),
+             "component functions, r_unit 0.01")
 
     if "simtrace" in groups:
         import importlib
