@@ -548,6 +548,10 @@ template <bool B>
 struct BoolC {
   static constexpr bool value = B;
 };
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
 
 template <int MAXN>
 struct LaneArrays {  // values of residents bumped inside the current candidate
@@ -716,7 +720,7 @@ k_place(PlanParams P) {
       aflags = c >> 8;
     }
     const bool exact = (P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY);
-    const bool margin = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
+    const bool margin_rt = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
     // the newcomer (planner.py:291-292)
 #if IGP_TIMING
     long long tm0 = clock64();
@@ -757,9 +761,12 @@ k_place(PlanParams P) {
     // lane 0 of warp 0 only (exact mode, to locate the first raising candidate).
     // serial and exact are compile-time per instantiation, so the common
     // pruned step carries none of the exact-mode bookkeeping
-    auto run_step = [&](auto serial_c, auto exact_c) {
+    auto run_step = [&](auto serial_c, auto exact_c, auto margin_c) {
       constexpr bool serial = decltype(serial_c)::value;
       constexpr bool exact = decltype(exact_c)::value;
+      // the pruned step also fixes the division shortcut's margin test
+      constexpr int MG = decltype(margin_c)::value;  // 0 off, 1 on, 2 runtime
+      const bool margin = MG == 2 ? margin_rt : MG == 1;
       int qhead = 0;
       int scan = 0;  // serial replay: next GPU index to test
       // cooperative mode: this lane's next candidate position; consecutive
@@ -815,7 +822,7 @@ k_place(PlanParams P) {
 
       while (true) {
         // warp-uniform stop (set by the serial replay's first raising candidate)
-        if (__any_sync(FULL, stop)) break;
+        if (serial && __any_sync(FULL, stop)) break;
         const unsigned idle = __ballot_sync(FULL, cj < 0) & take_mask;
 #ifndef IGP_REFILL_MIN
 #define IGP_REFILL_MIN 28
@@ -1170,8 +1177,9 @@ k_place(PlanParams P) {
       }
     };
 
-    if (exact) run_step(BoolC<false>{}, BoolC<true>{});
-    else run_step(BoolC<false>{}, BoolC<false>{});
+    if (exact) run_step(BoolC<false>{}, BoolC<true>{}, IntC<2>{});
+    else if (margin_rt) run_step(BoolC<false>{}, BoolC<false>{}, IntC<1>{});
+    else run_step(BoolC<false>{}, BoolC<false>{}, IntC<0>{});
 #if IGP_TIMING
     long long tm2 = clock64();
 #endif
@@ -1184,7 +1192,7 @@ k_place(PlanParams P) {
       // exact mode only: replay the step in the reference's candidate order to
       // find the first raising candidate and the PlanStats at that point
       st_evals = st_calls = st_cands = st_rres = st_run = 0;
-      if (wi == 0) run_step(BoolC<true>{}, BoolC<true>{});
+      if (wi == 0) run_step(BoolC<true>{}, BoolC<true>{}, IntC<2>{});
       if (t != 0) st_evals = st_calls = st_cands = st_rres = st_run = 0;
       tot_evals += st_evals;
       tot_calls += st_calls;
