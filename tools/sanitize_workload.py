@@ -31,4 +31,9 @@ rng = np.random.default_rng(1)
 ri = random_instance(rng, 4, hw)
 igp.alloc_gpus({s.name: s for s, _ in ri}, {s.name: c for s, c in ri}, hw, [], ri[0][0].name,
                igp.appropriate_batch(ri[0][0], hw), 0.05)
+simulate(igp.plan(inst[:4], hw), {s.name: s for s, _ in inst}, {s.name: c for s, c in inst}, hw,
+         SimConfig(300.0, 50.0), collect_trace=True)
+_device.components(wl[0][:, :64], np.arange(1, 65), np.full(64, 0.1), np.full(64, 0.5),
+                   np.arange(64) % 9, np.linspace(100.0, 500.0, 64), hv)
+igp.power_demand(hw, [50.0, 60.5, 70.25]); igp.power_demand(hw, [])
 print("sanitize workload done")
