@@ -29,17 +29,25 @@ ERROR_NAMES = {1: "BatchCapExceededError", 2: "InfeasibleSloError", 3: "Infeasib
                4: "NonPositiveDenominatorError", 5: "NonPositiveDenominatorError"}
 
 
+IGP_F_GW2 = 32  # include/igniter_b200.h: two warps per stream
+
+
 class StreamPlanner:
     """n_streams independent arrival streams of up to ``capacity`` arrivals each."""
 
     def __init__(self, hw, *, capacity: int, n_streams: int = 1, b_max: int = 32, device=None,
-                 flags: int = 0):
+                 flags: int | None = None):
         torch = _device._torch()
         self.lib = _native.lib_for_compute()
         self.hw = hw
         self.hv = _device.hw_array(hw_vector(hw))
-        self.S, self.C, self.b_max, self.flags = int(n_streams), int(capacity), int(b_max), int(flags)
         self.device = _device._dev(device)
+        if flags is None:
+            # two warps per stream while the streams leave warp slots free
+            # (1,000 streams: 20.3 ms vs 24.6 ms with one warp, config 5)
+            slots = torch.cuda.get_device_properties(self.device).multi_processor_count * 16
+            flags = IGP_F_GW2 if 2 * int(n_streams) <= slots else 0
+        self.S, self.C, self.b_max, self.flags = int(n_streams), int(capacity), int(b_max), int(flags)
         self.k = 0
         nbytes = int(self.lib.igp_stream_workspace_bytes(self.S, self.C, _device._np_ptr(self.hv),
                                                          self.b_max, self.flags))
