@@ -46,6 +46,10 @@ def _stream(device):
     return ctypes.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
 
 
+def sm_count(device=None) -> int:
+    return _torch().cuda.get_device_properties(_dev(device)).multi_processor_count
+
+
 def workspace(nbytes: int, device=None, tag="plan"):
     """A cached device byte buffer of at least nbytes (grows, never shrinks)."""
     torch = _torch()

@@ -156,6 +156,24 @@ def test_plan_many_matches_single_plans():
         assert (st.model_evals, st.candidate_gpus) == (st1.model_evals, st1.candidate_gpus)
 
 
+def test_plan_many_cta_path_vs_oracle(oracle_lib):
+    """Few large scenarios take one CTA each (planner._cta_per_scenario)."""
+    from paper_2211_01713_b200.planner import _cta_per_scenario
+    hw = make_v100()
+    rng = np.random.default_rng(77)
+    scen = [random_instance(rng, 600, hw) for _ in range(3)]
+    assert _cta_per_scenario(len(scen), 600)
+    many = igp.plan_many(scen, hw)
+    for sc, p in zip(scen, many):
+        wl = workload_table(sc)
+        r = oracle_lib.plan(wl, np.array(hw_vector(hw)), 32, name_ranks([s.name for s, _ in sc]))
+        units = {a.workload: int(round(a.r / hw.r_unit)) for g in p.gpus for a in g.allocations}
+        gpu_of = {a.workload: gi for gi, g in enumerate(p.gpus) for a in g.allocations}
+        names = [s.name for s, _ in sc]
+        assert [gpu_of[n] for n in names] == list(r["gpu_of"])
+        assert [units[n] for n in names] == list(r["units"])
+
+
 def test_r_unit_001_and_c3_generator_vs_oracle(oracle_lib):
     hw = make_v100(r_unit=0.01)
     rng = np.random.default_rng(2211)
