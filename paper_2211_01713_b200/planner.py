@@ -46,7 +46,8 @@ IGP_F_STATS = 1
 IGP_F_CTA = 4
 IGP_F_COOP = 16
 CTA_MIN_WORKLOADS = 512      # one CTA per plan: 12.6 ms vs 22.5 ms (one warp) at 1k workloads
-COOP_MIN_WORKLOADS = 5_000  # whole-GPU steps: 17.5 vs 20.1 us/step (one CTA) at 10k, 21 vs 157 at 100k
+COOP_MIN_WORKLOADS = 10_000  # whole-GPU steps: 16.2 vs 19.5 us/step (one CTA) at 15k, 16.8 vs 23.5 at 20k;
+                             # one CTA wins below 10k (13.1 vs 16.5 at 5k) and ties at 10k
 
 
 @dataclass
