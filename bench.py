@@ -11,8 +11,15 @@ the batch (prepare + place kernels).  Scenarios shard across ranks with no
 data-path collective (weak scaling); for N>1 the fixed-size plan records are
 gathered over NCCL inside the timed step.
 
+Parity inside the run: after the timed steps, rank 0 plans a spread subset of
+the SAME scenarios (first and last included) with the CPU oracle and asserts
+that GPU index, position, units and the _build_plan rows are bit-identical.
+The reference arm (--impl reference) plans that same subset, rebuilt from the
+same per-scenario seeds (synth.scenario_batch), on all host threads.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
+  (--gpus N > 1 without torchrun re-launches itself under torch.distributed.run)
 
 Prints ONE JSON line on rank 0.
 """
@@ -62,6 +69,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--check", type=int, default=16,
+                    help="scenarios of the batch checked bit-exact against the CPU oracle "
+                         "(at least the host thread count when the CPU baseline runs)")
     ap.add_argument("--flags", type=int, default=0, help="extra IGP_F_* flags")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram bytes per k_place launch from an ncu --set full capture of "
@@ -79,6 +89,48 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def batch_scenarios(sms: int) -> int:
+    """Scenarios per GPU per step: 16 per SM, one per resident warp slot."""
+    return sms * 16
+
+
+def check_indices(S: int, n: int) -> np.ndarray:
+    """n scenarios spread over the batch, the first and the last included."""
+    return np.unique(np.round(np.linspace(0, S - 1, max(2, min(n, S)))).astype(np.int64))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def bench_config(S: int, m: int, world: int) -> dict:
+    return {"workload": f"{S} scenarios x {m} workloads per GPU per step "
+                        "(C2 generator scaled to 10k, r_unit 0.025, b<=32, V100 profile; "
+                        "per-scenario seeds, synth.scenario_batch)",
+            "scenarios_per_gpu": S, "workloads_per_scenario": m,
+            "l2": "inputs larger than L2 (%.2f GB per GPU)" % (S * 16 * m * 8 / 1e9),
+            "parallelism": f"scenario shards x{world}, NCCL all-gather of plan records"}
+
+
+def spawn_ranks(args) -> None:
+    """--gpus N > 1 outside torchrun: re-launch under torch.distributed.run."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 class ClockSampler:
@@ -170,19 +222,31 @@ def fp64_peak():
     return lib.fp64_probe_flops(0, sms), lib.fp64_probe_flops(1, sms)
 
 
-def cpu_reference(wl, hw_vec, b_max, rank, threads, n_scen):
-    """The CPU oracle (restatement of the reference path) on host threads."""
+def cpu_reference(wl, hw_vec, b_max, rank, threads):
+    """The CPU oracle (restatement of the reference path, _build_plan rows
+    included) on host threads; returns (plans/s, seconds, outputs)."""
     from oracle import oracle
     oracle.build()
     t0 = time.perf_counter()
-    r = oracle.plan_batch(wl[:n_scen], hw_vec, b_max, rank, threads, stats=False)
+    r = oracle.plan_batch(wl, hw_vec, b_max, rank, threads, stats=True, pred=True)
     dt = time.perf_counter() - t0
     assert r["rc"] == 0
-    return n_scen / dt, dt
+    return wl.shape[0] / dt, dt, r
+
+
+def device_batch_size():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return batch_scenarios(torch.cuda.get_device_properties(0).multi_processor_count)
+    except Exception:  # noqa: BLE001 - the CPU arm also runs without a GPU
+        pass
+    return batch_scenarios(148)
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU path on all host threads (rank 0 only)."""
+    """--impl reference: the CPU path on all host threads (rank 0 only), on
+    the checked subset of the GPU arm's own batch (same seeds, same config)."""
     if rank != 0:
         return
     from paper_2211_01713_b200 import synth
@@ -190,18 +254,24 @@ def run_reference(args, rank, world):
     from paper_2211_01713_b200.planner import name_ranks
     hw = hardware()
     threads = args.cpu_threads or os.cpu_count() or 1
-    per_step = threads  # one 10k scenario per thread per step
-    wl, names = synth.scenarios(per_step, args.workloads, hw, seed=args.seed)
+    S = args.scenarios or device_batch_size()
+    idx = check_indices(S, max(args.check, threads))
+    wl, names = synth.scenario_batch(S, args.workloads, hw, seed=args.seed, indices=idx)
     rk = name_ranks(list(names))
     hv = np.array(hw_vector(hw))
     for _ in range(max(args.warmup, 0) and 1):
-        cpu_reference(wl, hv, 32, rk, threads, min(threads, per_step))
+        cpu_reference(wl[:threads], hv, 32, rk, threads)
     times = []
     for _ in range(args.steps):
-        _, dt = cpu_reference(wl, hv, 32, rk, threads, per_step)
+        _, dt, _ = cpu_reference(wl, hv, 32, rk, threads)
         times.append(dt)
     total = sum(times)
-    value = per_step * args.steps / total
+    n = len(idx)
+    value = n * args.steps / total
+    sample = (f"{n} of the {S} scenarios of the GPU arm's batch (indices "
+              f"{idx[0]}..{idx[-1]}, evenly spread, same per-scenario seeds) x {args.workloads} "
+              "workloads per step, plan() with _build_plan rows, one scenario per host thread "
+              "at a time (oracle/igniter_oracle.c, pthreads)")
     line = {
         "impl": "reference",
         "metric": "provisioning plans/sec at 10k workloads",
@@ -209,12 +279,9 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{per_step} scenarios x {args.workloads} workloads per step "
-                               "(C2 generator, r_unit 0.025, b<=32, V100 profile)",
-                   "workloads_per_scenario": args.workloads},
+        "config": bench_config(S, args.workloads, world),
         "cpu_baseline": {"value": value, "unit": "plans/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} x {args.workloads}-workload plans per step, one per "
-                                   "host thread (oracle/igniter_oracle.c, pthreads)"},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "plans/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,6 +290,10 @@ def run_reference(args, rank, world):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)  # does not return
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         if args.impl == "reference":
@@ -247,14 +318,17 @@ def main():
     b_max = 32
     m = args.workloads
     sms = torch.cuda.get_device_properties(device).multi_processor_count
-    S = args.scenarios or sms * 16
+    S = args.scenarios or batch_scenarios(sms)
     flags = args.flags
+    threads = args.cpu_threads or os.cpu_count() or 1
 
     # ---- synthetic inputs (different seed per rank: weak scaling) ----
-    wl_np, names = synth.scenarios(S, m, hw, seed=args.seed + 1000 * rank)
+    seed = args.seed + 1000 * rank
+    wl_np, names = synth.scenario_batch(S, m, hw, seed=seed)
     rk_np = name_ranks(list(names))
     wl_pin = torch.from_numpy(wl_np).pin_memory()
     rk_pin = torch.from_numpy(rk_np).pin_memory()
+    del wl_np
     d_wl = wl_pin.to(device)
     d_rk = rk_pin.to(device)
     i32 = torch.empty((5, S, m), dtype=torch.int32, device=device)
@@ -283,6 +357,7 @@ def main():
     ref_cands = int(st[:, 1].sum())
     ref_calls = int(st[:, 2].sum())
     ref_res_reads = int(st[:, 4].sum())
+    stats_exact = st.copy()
     gpus_exact = d_gc.cpu().numpy().copy()
     units_exact = i32[2].cpu().numpy().copy()
 
@@ -337,19 +412,54 @@ def main():
     value = S * world * args.steps / (ms_total / 1e3)
     evals_per_s = ref_model_evals * world * args.steps / (ms_total / 1e3)
 
+    # ---- parity of the timed steps' outputs (untimed): the CPU oracle on a
+    # spread subset of this batch, plus the CPU baseline timed on the same plans
+    dev_out = {"gpu_of": i32[0].cpu().numpy(), "pos": i32[1].cpu().numpy(),
+               "units": i32[2].cpu().numpy(), "gpu_count": d_gc.cpu().numpy()}
+    cpu = None
+    parity = None
+    if rank == 0 and args.check > 0:
+        idx = check_indices(S, args.check if args.no_cpu_baseline else max(args.check, threads))
+        wl_chk = wl_pin.numpy()[idx]
+        v, dt, o = cpu_reference(wl_chk, hv, b_max, rk_np, threads)
+        pred_chk = d_pred[torch.from_numpy(idx).to(device)].cpu().numpy()
+        for key in ("gpu_of", "pos", "units", "gpu_count"):
+            assert np.array_equal(dev_out[key][idx], o[key]), f"parity: {key} differs from the oracle"
+        assert np.array_equal(pred_chk.view(np.int64), o["pred"].view(np.int64)), \
+            "parity: _build_plan rows differ from the oracle"
+        assert np.array_equal(stats_exact[idx, 0], o["stats"][:, 0]), "parity: model_evals"
+        assert np.array_equal(stats_exact[idx, 1], o["stats"][:, 1]), "parity: candidate_gpus"
+        parity = {"scenarios_checked": [int(i) for i in idx], "oracle": "oracle/igniter_oracle.c",
+                  "fields": "gpu_of, pos, units, gpu_count, _build_plan rows (int64 bit patterns), "
+                            "PlanStats model_evals / candidate_gpus of the exact pass",
+                  "result": "bit-exact"}
+        if not args.no_cpu_baseline:
+            cpu = {"value": v, "unit": "plans/s", "cores": threads, "kind": "port",
+                   "cpu_model": cpu_model(),
+                   "sample": f"{len(idx)} of this batch's {S} scenarios (indices {idx[0]}..{idx[-1]}, "
+                             f"evenly spread) x {m}-workload plans with _build_plan rows, one per "
+                             f"host thread at a time, {dt:.1f} s (oracle/igniter_oracle.c "
+                             "restatement, pthreads)"}
+        del wl_chk, pred_chk, o
+
     # ---- e2e through the host-buffer C-ABI entry (pinned buffers, copies timed) ----
     e2e = None
+    e2e_launches = 0
     if not args.no_e2e:
         wl_host = wl_pin.numpy()
         rk_host = rk_pin.numpy()
         out = {k: torch.empty((S, m), dtype=torch.int32).pin_memory().numpy()
                for k in ("gpu_of", "pos", "units", "batch", "lb")}
+        out["pred"] = torch.empty((S, m, 10), dtype=torch.float64).pin_memory().numpy()
         out["gpu_count"] = torch.empty(S, dtype=torch.int32).pin_memory().numpy()
         out["stats"] = torch.empty((S, 6), dtype=torch.int64).pin_memory().numpy()
         out["err"] = np.zeros(S, _native.err_dtype())
         del ws
+        pred_ref = d_pred.cpu().numpy().view(np.int64) if rank == 0 else None
+        del d_pred, d_wl
         torch.cuda.empty_cache()
-        _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device, out=out)
+        _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device, want_pred=True,
+                          out=out)
         torch.cuda.synchronize()
         ea = torch.cuda.Event(enable_timing=True)
         eb = torch.cuda.Event(enable_timing=True)
@@ -357,7 +467,8 @@ def main():
             dist.barrier()
         ea.record(stream)
         for _ in range(args.steps):
-            _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device, out=out)
+            _device.plan_host(wl_host, hv, b_max, rk_host, flags=flags, device=device,
+                              want_pred=True, out=out)
         eb.record(stream)
         torch.cuda.synchronize()
         e2e_ms = ea.elapsed_time(eb)
@@ -366,12 +477,20 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         assert np.array_equal(out["units"], units_exact)
+        assert np.array_equal(out["gpu_of"], dev_out["gpu_of"])
+        if pred_ref is not None:
+            assert np.array_equal(out["pred"].view(np.int64), pred_ref)
         h2d = wl_host.nbytes + rk_host.nbytes
-        d2h = sum(out[k].nbytes for k in ("gpu_of", "pos", "units", "batch", "lb", "gpu_count",
-                                          "stats", "err"))
+        d2h = sum(out[k].nbytes for k in ("gpu_of", "pos", "units", "batch", "lb", "pred",
+                                          "gpu_count", "stats", "err"))
+        chunks = min(4, max(1, S // 128))
+        e2e_launches = KERNELS_PER_PLAN_CALL * chunks * args.steps
         e2e = {"value": S * world * args.steps / (e2e_ms / 1e3), "unit": "plans/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e2e_ms / args.steps}
+               "ms_per_step": e2e_ms / args.steps,
+               "path": f"igp_plan_batch_host (pinned host buffers; {chunks} scenario chunks on "
+                       "their own streams: H2D / kernels / D2H overlapped), _build_plan rows "
+                       "returned and checked equal to the device leg"}
 
     # ---- roofline of the dominant kernel (k_place, the place stage) ----
     # Both rooflines count the REFERENCE's work (exact-stats pass), not the
@@ -408,16 +527,6 @@ def main():
                             f"{FLOPS_PER_EVAL_CALL} x reference _eval_entries calls per launch",
     }
 
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        threads = args.cpu_threads or os.cpu_count() or 1
-        n = threads
-        wl_c, names_c = synth.scenarios(n, m, hw, seed=args.seed + 999_999)
-        v, dt = cpu_reference(wl_c, hv, b_max, name_ranks(list(names_c)), threads, n)
-        cpu = {"value": v, "unit": "plans/s", "cores": threads, "kind": "port",
-               "sample": f"{n} x {m}-workload plans, one per host thread, {dt:.1f} s "
-                         "(oracle/igniter_oracle.c restatement, pthreads)"}
-
     if rank == 0:
         line = {
             "metric": "provisioning plans/sec at 10k workloads",
@@ -425,11 +534,7 @@ def main():
             "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{S} scenarios x {m} workloads per GPU per step "
-                                  "(C2 generator scaled to 10k, r_unit 0.025, b<=32, V100 profile)",
-                       "scenarios_per_gpu": S, "workloads_per_scenario": m,
-                       "l2": "inputs larger than L2 (%.2f GB per GPU)" % (wl_np.nbytes / 1e9),
-                       "parallelism": f"scenario shards x{world}, NCCL all-gather of plan records"},
+            "config": bench_config(S, m, world),
             "candidate_evals_per_s": evals_per_s,
             "candidate_evals_definition": "reference PlanStats.model_evals (planner.py:156-157) "
                                           "of the planned scenarios, from an exact-stats pass",
@@ -438,8 +543,9 @@ def main():
                                                 "eval_calls": ref_calls,
                                                 "resident_reads": ref_res_reads,
                                                 "eval_calls_run_fast_path": performed_calls},
-            "gpu_launches": KERNELS_PER_PLAN_CALL * args.steps * (1 if args.no_e2e else 2),
+            "gpu_launches": KERNELS_PER_PLAN_CALL * args.steps + e2e_launches,
             "clocks": clocks,
+            "parity": parity,
             "roofline": roofline,
             "roofline_fp64": roofline_fp64,
             "cpu_baseline": cpu,

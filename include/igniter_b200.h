@@ -176,7 +176,15 @@ int igp_plan_place_device(const double *wl, int n_scen, int m, const double *hw,
 
 /* Same contract with HOST buffers: H2D copies, kernels, D2H copies and a
  * stream synchronisation all happen inside the call.  Pinned host memory is
- * recommended.  workspace is device memory of igp_plan_workspace_bytes(). */
+ * recommended.  workspace is device memory of igp_plan_host_workspace_bytes()
+ * (the planning scratch plus the device copies of the inputs and outputs),
+ * or workspace = NULL with workspace_bytes = 0: the library then allocates
+ * and frees it itself, stream-ordered (cudaMallocAsync / cudaFreeAsync).
+ * Batches of >= 256 scenarios are pipelined in up to four scenario chunks on
+ * library-owned streams ordered after `stream`: one chunk's kernels overlap
+ * the next chunk's H2D and the previous chunk's D2H copies. */
+size_t igp_plan_host_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags,
+                                     int rank_stride, int want_pred);
 int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw, int b_max,
                         const int32_t *name_rank, int rank_stride, int32_t *gpu_of,
                         int32_t *pos, int32_t *units, int32_t *batch, int32_t *lb,

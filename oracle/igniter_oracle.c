@@ -452,7 +452,8 @@ typedef struct {
   const double *hw;
   int b_max;
   const int32_t *name_rank;
-  int32_t *gpu_of, *units, *gpu_count;
+  int32_t *gpu_of, *pos, *units, *gpu_count;
+  double *pred; /* nullable: the _build_plan rows (planner.py:218-246) */
   int64_t *stats;
   int s_begin, s_end, rc;
 } batch_job_t;
@@ -465,8 +466,9 @@ static void *batch_worker(void *arg) {
   for (int s = j->s_begin; s < j->s_end; ++s) {
     igo_err e;
     int rc = igo_plan(j->wl + (int64_t)s * j->scen_stride, m, m, j->hw, j->b_max,
-                      j->name_rank, j->gpu_of + (int64_t)s * m, pos,
-                      j->units + (int64_t)s * m, bt, lb, NULL, j->gpu_count + s,
+                      j->name_rank, j->gpu_of + (int64_t)s * m,
+                      j->pos ? j->pos + (int64_t)s * m : pos, j->units + (int64_t)s * m, bt, lb,
+                      j->pred ? j->pred + (int64_t)s * m * 10 : NULL, j->gpu_count + s,
                       j->stats ? j->stats + 3 * s : NULL, &e);
     if (rc && !j->rc) j->rc = rc;
   }
@@ -477,8 +479,8 @@ static void *batch_worker(void *arg) {
 }
 
 int igo_plan_batch(const double *wl, int n_scen, int m, const double *hw, int b_max,
-                   const int32_t *name_rank, int32_t *gpu_of, int32_t *units,
-                   int32_t *gpu_count, int64_t *stats, int n_threads) {
+                   const int32_t *name_rank, int32_t *gpu_of, int32_t *pos, int32_t *units,
+                   double *pred, int32_t *gpu_count, int64_t *stats, int n_threads) {
   if (n_threads < 1) n_threads = 1;
   if (n_threads > n_scen) n_threads = n_scen > 0 ? n_scen : 1;
   pthread_t *th = malloc(sizeof(pthread_t) * n_threads);
@@ -487,7 +489,7 @@ int igo_plan_batch(const double *wl, int n_scen, int m, const double *hw, int b_
   for (int t = 0; t < n_threads; ++t) {
     int cnt = per + (t < extra);
     jobs[t] = (batch_job_t){wl, (int64_t)F_NF * m, m, hw, b_max, name_rank,
-                            gpu_of, units, gpu_count, stats, s0, s0 + cnt, 0};
+                            gpu_of, pos, units, gpu_count, pred, stats, s0, s0 + cnt, 0};
     s0 += cnt;
     pthread_create(&th[t], NULL, batch_worker, &jobs[t]);
   }

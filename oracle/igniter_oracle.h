@@ -30,8 +30,8 @@ int igo_plan(const double *wl, int64_t ld, int m, const double *hw, int b_max,
              int32_t *batch_out, int32_t *lb_out, double *pred, int32_t *gpu_count,
              int64_t *stats, igo_err *err);
 int igo_plan_batch(const double *wl, int n_scen, int m, const double *hw, int b_max,
-                   const int32_t *name_rank, int32_t *gpu_of, int32_t *units,
-                   int32_t *gpu_count, int64_t *stats, int n_threads);
+                   const int32_t *name_rank, int32_t *gpu_of, int32_t *pos, int32_t *units,
+                   double *pred, int32_t *gpu_count, int64_t *stats, int n_threads);
 int igo_solo_grid(const double *wl, int64_t ld, int m, const double *hw, int b_max,
                   int32_t *min_units, int64_t *n_evals);
 int igo_stream(const double *wl, int64_t ld, int n, const double *hw, int b_max,

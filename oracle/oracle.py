@@ -74,20 +74,25 @@ def plan(wl: np.ndarray, hw, b_max: int, rank: np.ndarray):
     return out
 
 
-def plan_batch(wl: np.ndarray, hw, b_max: int, rank: np.ndarray, threads: int, stats=False):
-    """S independent scenarios wl[S, 16, m] on `threads` host threads."""
+def plan_batch(wl: np.ndarray, hw, b_max: int, rank: np.ndarray, threads: int, stats=False,
+               pred=False):
+    """S independent scenarios wl[S, 16, m] on `threads` host threads; with
+    pred=True also the _build_plan rows (planner.py:218-246) and positions."""
     wl = np.ascontiguousarray(wl, np.float64)
     S, _, m = wl.shape
     hw = np.ascontiguousarray(hw, np.float64)
     rank = np.ascontiguousarray(rank, np.int32)
     gpu_of = np.zeros((S, m), np.int32)
     units = np.zeros((S, m), np.int32)
+    pos = np.zeros((S, m), np.int32) if pred else None
+    rows = np.zeros((S, m, 10)) if pred else None
     gc = np.zeros(S, np.int32)
     st = np.zeros((S, 3), np.int64) if stats else None
     rc = lib().igo_plan_batch(_p(wl), ctypes.c_int(S), ctypes.c_int(m), _p(hw), ctypes.c_int(b_max),
-                              _p(rank), _p(gpu_of), _p(units), _p(gc),
-                              _p(st) if stats else None, ctypes.c_int(threads))
-    return dict(gpu_of=gpu_of, units=units, gpu_count=gc, stats=st, rc=int(rc))
+                              _p(rank), _p(gpu_of), _p(pos) if pred else None, _p(units),
+                              _p(rows) if pred else None, _p(gc), _p(st) if stats else None,
+                              ctypes.c_int(threads))
+    return dict(gpu_of=gpu_of, pos=pos, units=units, pred=rows, gpu_count=gc, stats=st, rc=int(rc))
 
 
 def prologue(wl: np.ndarray, hw, b_max: int):

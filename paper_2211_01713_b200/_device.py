@@ -14,9 +14,6 @@ import numpy as np
 from . import _native
 from .layout import HW_NF, WL_NF
 
-_ws_cache: dict = {}
-
-
 def _torch():
     import torch
     return torch
@@ -51,16 +48,16 @@ def sm_count(device=None) -> int:
 
 
 def workspace(nbytes: int, device=None, tag="plan"):
-    """A cached device byte buffer of at least nbytes (grows, never shrinks)."""
+    """A device byte buffer of at least nbytes for one call.
+
+    Allocated per call through the torch caching allocator on the current
+    stream of `device`: the allocator recycles the block only after the work
+    queued on that stream, so concurrent calls from several threads or streams
+    never share scratch (the reference is pure Python and safe to call from
+    several threads; so is this)."""
     torch = _torch()
     device = _dev(device)
-    key = (str(device), tag)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < nbytes:
-        _ws_cache.pop(key, None)
-        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
-    return buf
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
 def hw_array(hw_vec) -> np.ndarray:
@@ -76,7 +73,14 @@ def _check(rc: int):
         from .errors import NativeError
         raise NativeError(
             "libigniter_b200 rejected the call "
-            + ("(capacity: max_units(hw) exceeds igp_max_cap())" if rc == 7 else "(bad argument)"))
+            + ("(capacity: max_units(hw) exceeds igp_max_cap() or m >= 2^23)" if rc == 7
+               else "(bad argument)"))
+
+
+def _pool_overflow():
+    from .errors import NativeError
+    return NativeError("libigniter_b200: a scenario outgrew the largest record pool "
+                       f"({POOL_RETRY} x m records)")
 
 
 def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
@@ -138,11 +142,14 @@ def _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred):
     return res
 
 
-def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=False, out=None):
+def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True, out=None):
     """Host-buffer entry (igp_plan_batch_host): H2D, kernels, D2H, sync in one call.
 
     `wl`/`rank` should be pinned (page-locked) numpy views for full PCIe
-    bandwidth; `out` may carry preallocated (pinned) output arrays."""
+    bandwidth; `out` may carry preallocated (pinned) output arrays.  Per-scenario
+    planning errors are left in out["err"] (codes 1-6, as plan_device); a
+    scenario whose tiles outgrow the default record pool is re-planned with the
+    pool size that suffices for any plan, like plan_device."""
     torch = _torch()
     lib = _native.lib_for_compute()
     device = _dev(device)
@@ -157,31 +164,35 @@ def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=False, ou
                    err=np.zeros(S, _native.err_dtype()))
         if want_pred:
             out["pred"] = np.empty((S, m, 10))
-    nbytes = host_workspace_bytes(S, m, h, b_max, flags, rank_stride, want_pred)
     with torch.cuda.device(device):
-        ws = workspace(nbytes, device, tag="host")
-        rc = lib.igp_plan_batch_host(
-            _np_ptr(wl), S, m, _np_ptr(h), int(b_max), _np_ptr(rank), rank_stride,
-            _np_ptr(out["gpu_of"]), _np_ptr(out["pos"]), _np_ptr(out["units"]),
-            _np_ptr(out["batch"]), _np_ptr(out["lb"]),
-            _np_ptr(out.get("pred")) if want_pred else ctypes.c_void_p(0),
-            _np_ptr(out["gpu_count"]), _np_ptr(out["stats"]), _np_ptr(out["err"]),
-            _ptr(ws), ws.numel(), int(flags), _stream(device))
-        if rc in (7, 8, 9):
-            _check(rc)
+        for attempt in range(2):
+            nbytes = host_workspace_bytes(S, m, h, b_max, flags, rank_stride, want_pred)
+            ws = workspace(nbytes, device)
+            rc = lib.igp_plan_batch_host(
+                _np_ptr(wl), S, m, _np_ptr(h), int(b_max), _np_ptr(rank), rank_stride,
+                _np_ptr(out["gpu_of"]), _np_ptr(out["pos"]), _np_ptr(out["units"]),
+                _np_ptr(out["batch"]), _np_ptr(out["lb"]),
+                _np_ptr(out.get("pred")) if want_pred else ctypes.c_void_p(0),
+                _np_ptr(out["gpu_count"]), _np_ptr(out["stats"]), _np_ptr(out["err"]),
+                _ptr(ws), ws.numel(), int(flags), _stream(device))
+            del ws
+            if rc in (8, 9):
+                _check(rc)
+            overflow = (out["err"]["code"] == 7).any()
+            if rc == 7 and not overflow:
+                _check(rc)  # a call-level limit, not a scenario's pool
+            if not overflow:
+                break
+            if attempt or ((flags >> 8) & 0xFF) >= POOL_RETRY:
+                raise _pool_overflow()
+            flags = (flags & ~0xFF00) | (POOL_RETRY << 8)
     return out
 
 
 def host_workspace_bytes(S, m, hw_vec, b_max, flags, rank_stride, want_pred):
-    base = plan_workspace_bytes(S, m, hw_vec, b_max, flags)
-    Sm = S * max(m, 1)
-
-    def al(x):
-        return (x + 255) & ~255
-    extra = al(Sm * WL_NF * 8) + al((Sm if rank_stride else max(m, 1)) * 4) + al(Sm * 20)
-    extra += al(Sm * 80 if want_pred else 0) + al(S * 4) + al(S * 48)
-    extra += al(S * ctypes.sizeof(_native.IgpError))
-    return base + extra + 4096
+    lib = _native.load()
+    return int(lib.igp_plan_host_workspace_bytes(S, m, _np_ptr(hw_array(hw_vec)), int(b_max),
+                                                 int(flags), int(rank_stride), int(bool(want_pred))))
 
 
 def eval_states(wl, batch, r, ptr, hw_vec, check_capacity=False, device=None):

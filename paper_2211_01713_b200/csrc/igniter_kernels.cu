@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "exact_fp64.cuh"
 
@@ -364,25 +365,38 @@ static size_t place_smem() {
   return (size_t)(GW == 1 ? 128 : GW * 32) * sizeof(LaneSlot);
 }
 
+// Per-device launch facts of one kernel instantiation: the opt-in dynamic
+// shared memory attribute is set, and the occupancy queried, once per device
+// ordinal (the attribute belongs to the device's context), under a lock.
+struct DevOcc {
+  int per_sm = -1, sms = 0;
+};
+template <typename Kern>
+static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static DevOcc cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  DevOcc &o = cache[dev & 63];
+  if (o.per_sm < 0) {
+    cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.per_sm, kern, threads, smem) !=
+            cudaSuccess ||
+        o.per_sm < 1)
+      o.per_sm = 1;
+  }
+  return o;
+}
+
 template <int MAXN, int GW>
 static unsigned place_grid(int S) {
   // persistent launch: at most as many groups as can be co-resident
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_place<MAXN, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)place_smem<GW>());
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place<MAXN, GW>,
-                                                      GW == 1 ? 128 : GW * 32,
-                                                      place_smem<GW>()) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-  }
+  const DevOcc o = dev_occupancy(k_place<MAXN, GW>, GW == 1 ? 128 : GW * 32, place_smem<GW>());
   const int gpb = (GW == 1) ? 4 : 1;
   const long long want = (S + gpb - 1) / gpb;
-  const long long cap = (long long)per_sm * sms;
+  const long long cap = (long long)o.per_sm * o.sms;
   return (unsigned)(want < cap ? want : cap);
 }
 
@@ -409,18 +423,8 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
 
 template <int MAXN>
 static int launch_place_coop(PlanParams P, cudaStream_t st) {
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_place<MAXN, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)place_smem<1>());
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_place<MAXN, 1, true>, 128,
-                                                      place_smem<1>()) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
-  }
+  const DevOcc o = dev_occupancy(k_place<MAXN, 1, true>, 128, place_smem<1>());
+  const int per_sm = o.per_sm, sms = o.sms;
   int grid = per_sm * sms;
   if (grid * 128 > COOP_MAX_LANES) grid = COOP_MAX_LANES / 128;
   // no more CTAs than the step's candidates can use (a step of m workloads has
@@ -561,6 +565,75 @@ int igp_plan_batch_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PA
 int igp_plan_prepare_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PASS, 1); }
 int igp_plan_place_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PASS, 2); }
 
+// igp_plan_batch_host pipelines the batch in up to HOST_CHUNKS scenario
+// chunks, each on its own stream with its own slice of the workspace: chunk
+// c's kernels overlap chunk c+1's H2D copy and chunk c-1's D2H copy, and the
+// chunks' persistent place kernels share the SMs (each is sized to a quarter
+// of the resident warp slots, so together they fill the GPU).
+static constexpr int HOST_CHUNKS = 4;
+static constexpr int HOST_CHUNK_MIN = 128;  // scenarios per chunk before splitting
+
+static int host_chunks(int n_scen, int flags) {
+  if (flags & IGP_F_COOP) return 1;
+  int nc = n_scen / HOST_CHUNK_MIN;
+  return nc < 1 ? 1 : nc > HOST_CHUNKS ? HOST_CHUNKS : nc;
+}
+
+struct HostChunkLayout {
+  size_t plan, o_wl, o_rank, o_i32, o_pred, o_gc, o_st, o_err, per_chunk;
+};
+
+static HostChunkLayout host_chunk_layout(int sc, int m, int cap, int flags, int rank_stride,
+                                         int want_pred) {
+  HostChunkLayout H;
+  const size_t Sm = (size_t)sc * (m > 0 ? m : 1);
+  const size_t rank_n = rank_stride ? Sm : (size_t)(m > 0 ? m : 1);
+  size_t off = ws_layout(sc, m, cap, flags).total;
+  H.plan = off;
+  H.o_wl = off; off = align_up(off + Sm * IGP_WL_NF * 8);
+  H.o_rank = off; off = align_up(off + rank_n * 4);
+  H.o_i32 = off; off = align_up(off + Sm * 4 * 5);
+  H.o_pred = off; off = align_up(off + (want_pred ? Sm * 80 : 0));
+  H.o_gc = off; off = align_up(off + (size_t)sc * 4);
+  H.o_st = off; off = align_up(off + (size_t)sc * 8 * IGP_NSTAT);
+  H.o_err = off; off = align_up(off + (size_t)sc * sizeof(igp_error));
+  H.per_chunk = off;
+  return H;
+}
+
+size_t igp_plan_host_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags,
+                                     int rank_stride, int want_pred) {
+  if (n_scen <= 0 || !hw) return 256;
+  Hw h = make_hw(hw, b_max);
+  const int nc = host_chunks(n_scen, flags);
+  const int sc = (n_scen + nc - 1) / nc;
+  return (size_t)nc * host_chunk_layout(sc, m, h.cap, flags, rank_stride, want_pred).per_chunk;
+}
+
+// per-thread, per-device chunk streams and events (created on first use)
+struct HostStreams {
+  int dev = -1;
+  cudaStream_t s[HOST_CHUNKS];
+  cudaEvent_t start, done[HOST_CHUNKS];
+};
+
+static int host_streams(HostStreams *&out) {
+  static thread_local HostStreams cache[8];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  HostStreams &h = cache[dev & 7];
+  if (h.dev != dev) {
+    for (int c = 0; c < HOST_CHUNKS; ++c) {
+      CK(cudaStreamCreateWithFlags(&h.s[c], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h.done[c], cudaEventDisableTiming));
+    }
+    CK(cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming));
+    h.dev = dev;
+  }
+  out = &h;
+  return IGP_E_OK;
+}
+
 int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h, int b_max,
                         const int32_t *name_rank, int rank_stride, int32_t *gpu_of, int32_t *pos,
                         int32_t *units, int32_t *batch, int32_t *lb, double *pred,
@@ -571,49 +644,78 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;
   if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
-  WsLayout L = ws_layout(n_scen, m, hw.cap, flags);
-  // device I/O buffers are carved after the planning scratch
-  size_t Sm = (size_t)n_scen * (m > 0 ? m : 1);
-  size_t rank_n = rank_stride ? Sm : (size_t)(m > 0 ? m : 1);
-  size_t off = L.total;
-  size_t o_wl = off; off = align_up(off + Sm * IGP_WL_NF * 8);
-  size_t o_rank = off; off = align_up(off + rank_n * 4);
-  size_t o_i32 = off; off = align_up(off + Sm * 4 * 5);
-  size_t o_pred = off; off = align_up(off + (pred ? Sm * 80 : 0));
-  size_t o_gc = off; off = align_up(off + (size_t)n_scen * 4);
-  size_t o_st = off; off = align_up(off + (size_t)n_scen * 8 * IGP_NSTAT);
-  size_t o_err = off; off = align_up(off + (size_t)n_scen * sizeof(igp_error));
-  if (!workspace || workspace_bytes < off) return IGP_E_ARG;
-  char *ws = (char *)workspace;
+  const int want_pred = pred != nullptr && !(flags & IGP_F_NO_PRED);
+  const int nc = host_chunks(n_scen, flags);
+  const int sc_max = (n_scen + nc - 1) / nc;
+  const HostChunkLayout H = host_chunk_layout(sc_max, m, hw.cap, flags, rank_stride, want_pred);
   cudaStream_t st = (cudaStream_t)stream;
-  double *d_wl = (double *)(ws + o_wl);
-  int32_t *d_rank = (int32_t *)(ws + o_rank);
-  int32_t *d_i32 = (int32_t *)(ws + o_i32);
-  double *d_pred = pred ? (double *)(ws + o_pred) : nullptr;
-  int32_t *d_gc = (int32_t *)(ws + o_gc);
-  int64_t *d_st = (int64_t *)(ws + o_st);
-  igp_error *d_err = (igp_error *)(ws + o_err);
-  if (m > 0) {
-    CK(cudaMemcpyAsync(d_wl, wl, Sm * IGP_WL_NF * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_rank, name_rank, rank_n * 4, cudaMemcpyHostToDevice, st));
+  void *owned = nullptr;  // workspace == NULL, bytes == 0: the library allocates it on the stream
+  if (!workspace && workspace_bytes == 0) {
+    CK(cudaMallocAsync(&owned, (size_t)nc * H.per_chunk, st));
+    workspace = owned;
+    workspace_bytes = (size_t)nc * H.per_chunk;
   }
-  int rc = igp_plan_batch_device(d_wl, n_scen, m, hw_h, b_max, d_rank, rank_stride, d_i32,
-                                 d_i32 + Sm, d_i32 + 2 * Sm, d_i32 + 3 * Sm, d_i32 + 4 * Sm, d_pred,
-                                 d_gc, stats ? d_st : nullptr, d_err, workspace, L.total, flags,
-                                 stream);
-  if (rc) return rc;
-  if (m > 0) {
-    if (gpu_of) CK(cudaMemcpyAsync(gpu_of, d_i32, Sm * 4, cudaMemcpyDeviceToHost, st));
-    if (pos) CK(cudaMemcpyAsync(pos, d_i32 + Sm, Sm * 4, cudaMemcpyDeviceToHost, st));
-    if (units) CK(cudaMemcpyAsync(units, d_i32 + 2 * Sm, Sm * 4, cudaMemcpyDeviceToHost, st));
-    if (batch) CK(cudaMemcpyAsync(batch, d_i32 + 3 * Sm, Sm * 4, cudaMemcpyDeviceToHost, st));
-    if (lb) CK(cudaMemcpyAsync(lb, d_i32 + 4 * Sm, Sm * 4, cudaMemcpyDeviceToHost, st));
-    if (pred) CK(cudaMemcpyAsync(pred, d_pred, Sm * 80, cudaMemcpyDeviceToHost, st));
+  if (!workspace || workspace_bytes < (size_t)nc * H.per_chunk) return IGP_E_ARG;
+  HostStreams *hs = nullptr;
+  if (nc > 1) {
+    int rc = host_streams(hs);
+    if (rc) return rc;
+    CK(cudaEventRecord(hs->start, st));  // the chunks follow the caller's prior work
   }
-  CK(cudaMemcpyAsync(gpu_count, d_gc, (size_t)n_scen * 4, cudaMemcpyDeviceToHost, st));
-  if (stats)
-    CK(cudaMemcpyAsync(stats, d_st, (size_t)n_scen * 8 * IGP_NSTAT, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(err, d_err, (size_t)n_scen * sizeof(igp_error), cudaMemcpyDeviceToHost, st));
+  const size_t mm = (size_t)(m > 0 ? m : 1);
+  for (int c = 0; c < nc; ++c) {
+    const int s0 = c * sc_max;
+    const int sc = (n_scen - s0) < sc_max ? (n_scen - s0) : sc_max;
+    if (sc <= 0) break;
+    cudaStream_t cs = st;
+    if (nc > 1) {
+      cs = hs->s[c];
+      CK(cudaStreamWaitEvent(cs, hs->start, 0));
+    }
+    char *ws = (char *)workspace + (size_t)c * H.per_chunk;
+    const size_t Sm = (size_t)sc * mm, Sm0 = (size_t)s0 * mm;
+    const size_t rank_n = rank_stride ? Sm : mm;
+    double *d_wl = (double *)(ws + H.o_wl);
+    int32_t *d_rank = (int32_t *)(ws + H.o_rank);
+    int32_t *d_i32 = (int32_t *)(ws + H.o_i32);
+    double *d_pred = want_pred ? (double *)(ws + H.o_pred) : nullptr;
+    int32_t *d_gc = (int32_t *)(ws + H.o_gc);
+    int64_t *d_st = (int64_t *)(ws + H.o_st);
+    igp_error *d_err = (igp_error *)(ws + H.o_err);
+    if (m > 0) {
+      CK(cudaMemcpyAsync(d_wl, wl + Sm0 * IGP_WL_NF, Sm * IGP_WL_NF * 8, cudaMemcpyHostToDevice,
+                         cs));
+      CK(cudaMemcpyAsync(d_rank, name_rank + (rank_stride ? Sm0 : 0), rank_n * 4,
+                         cudaMemcpyHostToDevice, cs));
+    }
+    int rc = igp_plan_batch_device(d_wl, sc, m, hw_h, b_max, d_rank, rank_stride, d_i32,
+                                   d_i32 + Sm, d_i32 + 2 * Sm, d_i32 + 3 * Sm, d_i32 + 4 * Sm,
+                                   d_pred, d_gc, stats ? d_st : nullptr, d_err, ws, H.plan, flags,
+                                   cs);
+    if (rc) return rc;
+    if (m > 0) {
+      if (gpu_of) CK(cudaMemcpyAsync(gpu_of + Sm0, d_i32, Sm * 4, cudaMemcpyDeviceToHost, cs));
+      if (pos) CK(cudaMemcpyAsync(pos + Sm0, d_i32 + Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+      if (units)
+        CK(cudaMemcpyAsync(units + Sm0, d_i32 + 2 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+      if (batch)
+        CK(cudaMemcpyAsync(batch + Sm0, d_i32 + 3 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+      if (lb) CK(cudaMemcpyAsync(lb + Sm0, d_i32 + 4 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+      if (want_pred)
+        CK(cudaMemcpyAsync(pred + Sm0 * 10, d_pred, Sm * 80, cudaMemcpyDeviceToHost, cs));
+    }
+    CK(cudaMemcpyAsync(gpu_count + s0, d_gc, (size_t)sc * 4, cudaMemcpyDeviceToHost, cs));
+    if (stats)
+      CK(cudaMemcpyAsync(stats + (size_t)s0 * IGP_NSTAT, d_st, (size_t)sc * 8 * IGP_NSTAT,
+                         cudaMemcpyDeviceToHost, cs));
+    CK(cudaMemcpyAsync(err + s0, d_err, (size_t)sc * sizeof(igp_error), cudaMemcpyDeviceToHost,
+                       cs));
+    if (nc > 1) {
+      CK(cudaEventRecord(hs->done[c], cs));
+      CK(cudaStreamWaitEvent(st, hs->done[c], 0));
+    }
+  }
+  if (owned) CK(cudaFreeAsync(owned, st));
   CK(cudaStreamSynchronize(st));
   for (int s = 0; s < n_scen; ++s)
     if (err[s].code) return err[s].code;

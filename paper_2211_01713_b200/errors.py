@@ -76,6 +76,53 @@ class ProblemFormatError(GpuPlannerError):
     """Malformed input document (API parity only)."""
 
 
+def _reference_errors():
+    """The reference's ``gpuplanner.errors`` module when it is importable in
+    this process and is not this package under an alias, else None."""
+    import importlib
+    import importlib.util
+    import os
+    import sys
+    if os.environ.get("IGP_OWN_ERRORS"):
+        return None
+    here = os.path.dirname(os.path.abspath(__file__))
+    mod = sys.modules.get("gpuplanner.errors")
+    if mod is None:
+        top = sys.modules.get("gpuplanner")
+        if top is not None and os.path.dirname(os.path.abspath(getattr(top, "__file__", "") or
+                                                                "/")) == here:
+            return None
+        try:
+            spec = importlib.util.find_spec("gpuplanner")
+        except (ImportError, ValueError):
+            return None
+        if spec is None or (spec.origin and os.path.dirname(os.path.abspath(spec.origin)) == here):
+            return None
+        try:
+            mod = importlib.import_module("gpuplanner.errors")
+        except Exception:  # noqa: BLE001 - a broken reference install: keep our own classes
+            return None
+    path = getattr(mod, "__file__", None)
+    if not path or os.path.dirname(os.path.abspath(path)) == here:
+        return None
+    return mod
+
+
+# When the reference package is importable, its exception classes ARE this
+# package's: `except gpuplanner.errors.PlanningError` written against the
+# reference keeps catching what this package raises (class identity, not just
+# names).  Our definitions above are the same hierarchy for when it is not.
+_REF = _reference_errors()
+if _REF is not None:
+    for _n in ("GpuPlannerError", "NonPositiveDenominatorError", "OverAllocatedError",
+               "InsufficientDataError", "DegenerateDesignError", "ZeroVarianceError",
+               "PlanningError", "InfeasibleSloError", "InfeasibleResourceError",
+               "BatchCapExceededError", "InfeasibleError", "BudgetExceededError",
+               "UnstableQueueError", "ProblemFormatError"):
+        if hasattr(_REF, _n):
+            globals()[_n] = getattr(_REF, _n)
+
+
 class NativeError(GpuPlannerError):
     """The CUDA library failed for a reason that has no reference counterpart."""
 

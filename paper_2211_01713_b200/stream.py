@@ -62,9 +62,10 @@ class StreamPlanner:
         return _device._stream(self.device)
 
     def reset(self):
-        rc = self.lib.igp_stream_reset_device(self.S, self.C, _device._np_ptr(self.hv), self.b_max,
-                                              _device._ptr(self.ws), self.ws.numel(), self.flags,
-                                              self._stream())
+        with _device._torch().cuda.device(self.device):
+            rc = self.lib.igp_stream_reset_device(self.S, self.C, _device._np_ptr(self.hv),
+                                                  self.b_max, _device._ptr(self.ws),
+                                                  self.ws.numel(), self.flags, self._stream())
         _device._check(rc)
         self.k = 0
 
@@ -78,11 +79,12 @@ class StreamPlanner:
         if self.k + n > self.C:
             raise ValueError(f"stream capacity {self.C} exceeded ({self.k} + {n})")
         out = self._out.view(-1)[: 3 * self.S * n].view(3, self.S, n)
-        rc = self.lib.igp_stream_push_device(
-            _device._ptr(wl_new), self.S, self.k, n, self.C, _device._np_ptr(self.hv), self.b_max,
-            _device._ptr(out[0]), _device._ptr(out[1]), _device._ptr(out[2]),
-            _device._ptr(self.stats), _device._ptr(self.err), _device._ptr(self.ws),
-            self.ws.numel(), self.flags, self._stream())
+        with _device._torch().cuda.device(self.device):
+            rc = self.lib.igp_stream_push_device(
+                _device._ptr(wl_new), self.S, self.k, n, self.C, _device._np_ptr(self.hv),
+                self.b_max, _device._ptr(out[0]), _device._ptr(out[1]), _device._ptr(out[2]),
+                _device._ptr(self.stats), _device._ptr(self.err), _device._ptr(self.ws),
+                self.ws.numel(), self.flags, self._stream())
         _device._check(rc)
         self.k += n
         return out[0], out[1], out[2]

@@ -78,3 +78,27 @@ def scenarios(n_scen: int, m: int, hw, seed: int = 0, *, slo=(20.0, 80.0),
     wl[...] = flat.reshape(WL_NF, n_scen, m).transpose(1, 0, 2)
     names = np.array([f"w{i:04d}" for i in range(m)])
     return wl, names
+
+
+def scenario_batch(n_scen: int, m: int, hw, seed: int = 0, *, indices=None,
+                   slo=(20.0, 80.0), rate=(50.0, 500.0), b_max: int = 32):
+    """Like ``scenarios`` but scenario s draws from its own stream
+    (``SeedSequence([seed, s])``), so any subset of a batch can be rebuilt
+    on its own: ``indices`` selects the scenarios to return (default: all
+    n_scen).  The benchmark's GPU arm plans the whole batch and its CPU arms
+    plan, and check, a subset of the SAME scenarios."""
+    idx = range(n_scen) if indices is None else [int(i) for i in indices]
+    wl = np.empty((len(idx), WL_NF, m), dtype=np.float64)
+    for o, s in enumerate(idx):
+        if not 0 <= s < n_scen:
+            raise IndexError(f"scenario {s} outside the batch of {n_scen}")
+        rng = np.random.default_rng(np.random.SeedSequence([seed, s]))
+        filled = 0
+        while filled < m:
+            cand = _draw(rng, int((m - filled) * 1.6) + 64, slo, rate)
+            good = cand[:, _feasible(cand, hw, b_max)]
+            take = min(m - filled, good.shape[1])
+            wl[o, :, filled:filled + take] = good[:, :take]
+            filled += take
+    names = np.array([f"w{i:04d}" for i in range(m)])
+    return wl, names

@@ -1,0 +1,65 @@
+"""The reference's own test-suite, run against this package on the B200.
+
+``support.py``, ``test_planner.py``, ``test_model.py`` and
+``test_model_properties.py`` in this directory are unmodified copies of
+``/root/reference/pkg/tests/`` (the reference's API contract for the planning
+and prediction path; the calibration and baseline tests are outside the
+path).  They import ``gpuplanner``; this conftest makes that name resolve to
+``paper_2211_01713_b200`` -- the import swap a user of the reference makes --
+with ``gpuplanner.problem`` served by ``paper_2211_01713_b200.document``.
+Every computation the tests trigger runs in the sm_100a library, so all of
+them are GPU tests.
+
+``test_inference_latency_monotone_in_resources`` is a property the
+reference's model does not always satisfy (hypothesis finds counterexamples
+in the reference itself); it is a non-strict xfail here as it
+is a flaky test there.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+if HERE not in sys.path:
+    sys.path.insert(0, HERE)
+
+import paper_2211_01713_b200 as _pkg  # noqa: E402
+from paper_2211_01713_b200 import document, errors, model, planner  # noqa: E402
+
+for _name, _mod in {"gpuplanner": _pkg, "gpuplanner.errors": errors,
+                    "gpuplanner.model": model, "gpuplanner.planner": planner,
+                    "gpuplanner.problem": document}.items():
+    sys.modules[_name] = _mod
+
+from support import demo_coef, demo_spec, make_v100  # noqa: E402
+
+FLAKY_IN_REFERENCE = {"test_inference_latency_monotone_in_resources"}
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        if not str(item.fspath).startswith(HERE + os.sep):
+            continue
+        item.add_marker(pytest.mark.gpu)
+        if item.originalname in FLAKY_IN_REFERENCE:
+            item.add_marker(pytest.mark.xfail(
+                strict=False, reason="model property the reference itself violates"))
+
+
+@pytest.fixture
+def v100():
+    return make_v100()
+
+
+@pytest.fixture
+def spec():
+    return demo_spec()
+
+
+@pytest.fixture
+def coef():
+    return demo_coef()
