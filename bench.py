@@ -453,7 +453,7 @@ def main():
         out["pred"] = torch.empty((S, m, 10), dtype=torch.float64).pin_memory().numpy()
         out["gpu_count"] = torch.empty(S, dtype=torch.int32).pin_memory().numpy()
         out["stats"] = torch.empty((S, 6), dtype=torch.int64).pin_memory().numpy()
-        out["err"] = np.zeros(S, _native.err_dtype())
+        out["err"] = torch.zeros(S * _native.err_dtype().itemsize, dtype=torch.uint8).pin_memory().numpy().view(_native.err_dtype())
         del ws
         pred_ref = d_pred.cpu().numpy().view(np.int64) if rank == 0 else None
         del d_pred, d_wl

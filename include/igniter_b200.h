@@ -114,10 +114,16 @@ enum {
                            lower latency for single large plans */
   IGP_F_GW2 = 32,       /* two / four warps per scenario (between the default one */
   IGP_F_GW4 = 64,       /* warp and IGP_F_CTA's eight) */
-  IGP_F_COOP = 16       /* single scenario (n_scen == 1): every warp of the GPU
+  IGP_F_COOP = 16,      /* single scenario (n_scen == 1): every warp of the GPU
                            shares each step (grid-cooperative launch); falls back
                            on the device to IGP_F_CTA when the exact sequence is
                            needed (IGP_F_STATS, or a scenario that can raise) */
+  IGP_F_HWS = 128       /* one hardware profile per scenario: hw points to
+                           n_scen x IGP_HW_NF doubles (host) instead of one
+                           profile.  select_gpu_type (planner.py:333-364) plans
+                           every GPU type of a request as one scenario of ONE
+                           launch.  Not combined with IGP_F_COOP or the stream
+                           entry points. */
 };
 
 int igp_abi_version(void);
@@ -126,7 +132,8 @@ int igp_max_cap(void);
 /* last CUDA error string of this thread (for IGP_E_CUDA) */
 const char *igp_last_error_string(void);
 
-/* Device workspace needed by igp_plan_batch_*() for S scenarios of m workloads. */
+/* Device workspace needed by igp_plan_batch_*() for S scenarios of m workloads
+ * (hw: one profile, or n_scen profiles with IGP_F_HWS). */
 size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags);
 
 /*
@@ -233,6 +240,11 @@ int igp_prologue_device(const double *wl, int m, const double *hw, int b_max,
  * together; each push appends n arrivals to every stream.  All state lives in
  * the caller's device workspace (igp_stream_workspace_bytes); the caller
  * tracks k0 = arrivals pushed so far.
+ *   flags:     a single stream (n_streams == 1) may run a push with
+ *              IGP_F_COOP: every warp of the GPU shares each arrival's step
+ *              (bits 16..27 of flags: the CTA count, 0 = whole GPU); the
+ *              per-CTA kernel resumes at the first arrival that needs the
+ *              exact sequence.  Pushes with and without it mix freely.
  *   push:      wl_new [S][16][n]; outputs [S][n]: GPU index and position
  *              within that GPU at admission (-1 when rejected), and the code
  *              (IGP_E_* in the low 8 bits); err [S] (device, nullable): a

@@ -60,10 +60,18 @@ def workspace(nbytes: int, device=None, tag="plan"):
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
 
 
+IGP_F_HWS = 128  # include/igniter_b200.h: one hardware profile per scenario
+
+
 def hw_array(hw_vec) -> np.ndarray:
+    """One profile [HW_NF], or one per scenario [S, HW_NF] (IGP_F_HWS)."""
     h = np.ascontiguousarray(np.asarray(hw_vec, dtype=np.float64))
-    assert h.shape == (HW_NF,)
+    assert h.shape[-1] == HW_NF and h.ndim in (1, 2)
     return h
+
+
+def _hw_flags(h, flags):
+    return flags | IGP_F_HWS if h.ndim == 2 else flags
 
 
 def _check(rc: int):
@@ -86,7 +94,7 @@ def _pool_overflow():
 def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
     lib = _native.load()
     h = hw_array(hw_vec)
-    return int(lib.igp_plan_workspace_bytes(S, m, _np_ptr(h), b_max, flags))
+    return int(lib.igp_plan_workspace_bytes(S, m, _np_ptr(h), b_max, _hw_flags(h, flags)))
 
 
 POOL_RETRY = 14  # tiles 4m + 8G <= 12m records plus <= 2m header slots always suffice
@@ -117,6 +125,8 @@ def _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred):
     rank = np.asarray(rank, dtype=np.int32)
     rank_stride = m if rank.ndim == 2 else 0
     h = hw_array(hw_vec)
+    assert h.ndim == 1 or h.shape[0] == S, "one hardware profile per scenario"
+    flags = _hw_flags(h, flags)
     with torch.cuda.device(device):
         d_wl = _to_dev(wl, device)
         d_rank = _to_dev(rank, device)
@@ -156,6 +166,7 @@ def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True, out
     S, nf, m = wl.shape
     rank_stride = m if rank.ndim == 2 else 0
     h = hw_array(hw_vec)
+    flags = _hw_flags(h, flags)
     if out is None:
         out = dict(gpu_of=np.empty((S, m), np.int32), pos=np.empty((S, m), np.int32),
                    units=np.empty((S, m), np.int32), batch=np.empty((S, m), np.int32),
@@ -191,8 +202,10 @@ def plan_host(wl, hw_vec, b_max, rank, flags=0, device=None, want_pred=True, out
 
 def host_workspace_bytes(S, m, hw_vec, b_max, flags, rank_stride, want_pred):
     lib = _native.load()
-    return int(lib.igp_plan_host_workspace_bytes(S, m, _np_ptr(hw_array(hw_vec)), int(b_max),
-                                                 int(flags), int(rank_stride), int(bool(want_pred))))
+    h = hw_array(hw_vec)
+    return int(lib.igp_plan_host_workspace_bytes(S, m, _np_ptr(h), int(b_max),
+                                                 int(_hw_flags(h, flags)), int(rank_stride),
+                                                 int(bool(want_pred))))
 
 
 def eval_states(wl, batch, r, ptr, hw_vec, check_capacity=False, device=None):

@@ -24,8 +24,11 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <vector>
 
 #include "exact_fp64.cuh"
 
@@ -374,11 +377,11 @@ struct DevOcc {
 template <typename Kern>
 static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
   static std::mutex mu;
-  static DevOcc cache[64];
+  static std::map<std::pair<const void *, int>, DevOcc> cache;  // (kernel, device)
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(mu);
-  DevOcc &o = cache[dev & 63];
+  DevOcc &o = cache[{(const void *)kern, dev}];
   if (o.per_sm < 0) {
     cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -390,10 +393,11 @@ static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
   return o;
 }
 
-template <int MAXN, int GW>
+template <int MAXN, int GW, bool HWS = false>
 static unsigned place_grid(int S) {
   // persistent launch: at most as many groups as can be co-resident
-  const DevOcc o = dev_occupancy(k_place<MAXN, GW>, GW == 1 ? 128 : GW * 32, place_smem<GW>());
+  const DevOcc o = dev_occupancy(k_place<MAXN, GW, false, HWS>, GW == 1 ? 128 : GW * 32,
+                                 place_smem<GW>());
   const int gpb = (GW == 1) ? 4 : 1;
   const long long want = (S + gpb - 1) / gpb;
   const long long cap = (long long)o.per_sm * o.sms;
@@ -403,6 +407,15 @@ static unsigned place_grid(int S) {
 template <int MAXN>
 static void launch_place(const PlanParams &P, cudaStream_t st) {
   cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
+  if (P.hw_s) {  // one profile per scenario: one CTA or one warp per scenario
+    if (P.flags & IGP_F_CTA)
+      k_place<MAXN, 8, false, true>
+          <<<place_grid<MAXN, 8, true>(P.S), 256, place_smem<8>(), st>>>(P);
+    else
+      k_place<MAXN, 1, false, true>
+          <<<place_grid<MAXN, 1, true>(P.S), 128, place_smem<1>(), st>>>(P);
+    return;
+  }
   if (P.flags & IGP_F_CTA) {
     k_place<MAXN, 8><<<place_grid<MAXN, 8>(P.S), 256, place_smem<8>(), st>>>(P);
   } else if (P.flags & IGP_F_GW4) {
@@ -434,9 +447,12 @@ static int launch_place_coop(PlanParams P, cudaStream_t st) {
   const int lim = want_ctas ? want_ctas : (by_m > 1 ? by_m : 1);
   if (grid > lim) grid = lim;
   CK(cudaMemsetAsync(P.coop, 0, sizeof(CoopState), st));
-  // the slack order starts empty before any warp reads it (the kernel has no
-  // grid-wide barrier before its first step)
-  CK(cudaMemsetAsync(P.sE, 0, sizeof(int32_t) * (P.hw.cap + 2), st));
+  // plan mode: the slack order starts empty before any warp reads it (the
+  // kernel has no grid-wide barrier before its first step); stream mode: it
+  // persists, and so does the pool top
+  if (!P.stream) CK(cudaMemsetAsync(P.sE, 0, sizeof(int32_t) * (P.hw.cap + 2), st));
+  else CK(cudaMemcpyAsync(&P.coop->pool_top, P.sstate + 1, sizeof(int32_t),
+                          cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(P.coop->best, 0xff, sizeof(P.coop->best), st));
   void *args[] = {&P};
   CK(cudaLaunchCooperativeKernel((const void *)k_place<MAXN, 1, true>, dim3(grid), dim3(128), args,
@@ -451,9 +467,19 @@ int igp_abi_version(void) { return IGP_ABI_VERSION; }
 int igp_max_cap(void) { return 256; }
 const char *igp_last_error_string(void) { return g_last_err; }
 
+// The largest max_units over the call's profiles (one, or n_scen with IGP_F_HWS).
+static int cap_of(const double *hw, int n_scen, int b_max, int flags) {
+  int cap = make_hw(hw, b_max).cap;
+  if (flags & IGP_F_HWS)
+    for (int s = 1; s < n_scen; ++s) {
+      const int c = make_hw(hw + (size_t)s * IGP_HW_NF, b_max).cap;
+      if (c > cap) cap = c;
+    }
+  return cap;
+}
+
 size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags) {
-  Hw h = make_hw(hw, b_max);
-  return ws_layout(n_scen, m, h.cap, flags).total;
+  return ws_layout(n_scen, m, cap_of(hw, n_scen, b_max, flags), flags).total;
 }
 
 static int plan_device_impl(const double *wl, int n_scen, int m, const double *hw_h, int b_max,
@@ -464,7 +490,17 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
                             int stages) {
   if (n_scen < 0 || m < 0 || !hw_h) return IGP_E_ARG;
   if (n_scen == 0) return IGP_E_OK;
+  if ((flags & IGP_F_HWS) && (flags & IGP_F_COOP)) return IGP_E_ARG;
   Hw hw = make_hw(hw_h, b_max);
+  std::vector<Hw> hws;
+  if (flags & IGP_F_HWS) {
+    hws.resize(n_scen);
+    for (int s = 0; s < n_scen; ++s) {
+      hws[s] = make_hw(hw_h + (size_t)s * IGP_HW_NF, b_max);
+      if (hws[s].cap < 1) return IGP_E_ARG;
+      if (hws[s].cap > hw.cap) hw.cap = hws[s].cap;  // layout / dispatch size
+    }
+  }
   if (hw.cap < 1) return IGP_E_ARG;
   if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
   if (m >= (1 << 23)) return IGP_E_CAPACITY;  // candidate keys pack j into 23 bits
@@ -474,6 +510,14 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   char *ws = (char *)workspace;
   PlanParams P;
   P.hw = hw;
+  P.hw_s = nullptr;
+  P.cap_ld = hw.cap;
+  if (flags & IGP_F_HWS) {
+    // pageable source: the copy is staged before cudaMemcpyAsync returns
+    CK(cudaMemcpyAsync(ws + L.hws, hws.data(), hws.size() * sizeof(Hw), cudaMemcpyHostToDevice,
+                       st));
+    P.hw_s = (const Hw *)(ws + L.hws);
+  }
   P.S = n_scen;
   P.m = m;
   P.flags = flags;
@@ -576,6 +620,7 @@ static constexpr int HOST_CHUNK_MIN = 128;  // scenarios per chunk before splitt
 static int host_chunks(int n_scen, int flags) {
   if (flags & IGP_F_COOP) return 1;
   int nc = n_scen / HOST_CHUNK_MIN;
+  if (const char *e = getenv("IGP_HOST_CHUNKS")) nc = atoi(e);  // A/B experiments
   return nc < 1 ? 1 : nc > HOST_CHUNKS ? HOST_CHUNKS : nc;
 }
 
@@ -604,10 +649,10 @@ static HostChunkLayout host_chunk_layout(int sc, int m, int cap, int flags, int 
 size_t igp_plan_host_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags,
                                      int rank_stride, int want_pred) {
   if (n_scen <= 0 || !hw) return 256;
-  Hw h = make_hw(hw, b_max);
   const int nc = host_chunks(n_scen, flags);
   const int sc = (n_scen + nc - 1) / nc;
-  return (size_t)nc * host_chunk_layout(sc, m, h.cap, flags, rank_stride, want_pred).per_chunk;
+  return (size_t)nc * host_chunk_layout(sc, m, cap_of(hw, n_scen, b_max, flags), flags,
+                                        rank_stride, want_pred).per_chunk;
 }
 
 // per-thread, per-device chunk streams and events (created on first use)
@@ -642,6 +687,7 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
   if (n_scen < 0 || m < 0 || !hw_h) return IGP_E_ARG;
   if (n_scen == 0) return IGP_E_OK;
   Hw hw = make_hw(hw_h, b_max);
+  hw.cap = cap_of(hw_h, n_scen, b_max, flags);
   if (hw.cap < 1) return IGP_E_ARG;
   if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
   const int want_pred = pred != nullptr && !(flags & IGP_F_NO_PRED);
@@ -663,56 +709,63 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
     CK(cudaEventRecord(hs->start, st));  // the chunks follow the caller's prior work
   }
   const size_t mm = (size_t)(m > 0 ? m : 1);
-  for (int c = 0; c < nc; ++c) {
-    const int s0 = c * sc_max;
-    const int sc = (n_scen - s0) < sc_max ? (n_scen - s0) : sc_max;
-    if (sc <= 0) break;
-    cudaStream_t cs = st;
-    if (nc > 1) {
-      cs = hs->s[c];
-      CK(cudaStreamWaitEvent(cs, hs->start, 0));
-    }
-    char *ws = (char *)workspace + (size_t)c * H.per_chunk;
-    const size_t Sm = (size_t)sc * mm, Sm0 = (size_t)s0 * mm;
-    const size_t rank_n = rank_stride ? Sm : mm;
-    double *d_wl = (double *)(ws + H.o_wl);
-    int32_t *d_rank = (int32_t *)(ws + H.o_rank);
-    int32_t *d_i32 = (int32_t *)(ws + H.o_i32);
-    double *d_pred = want_pred ? (double *)(ws + H.o_pred) : nullptr;
-    int32_t *d_gc = (int32_t *)(ws + H.o_gc);
-    int64_t *d_st = (int64_t *)(ws + H.o_st);
-    igp_error *d_err = (igp_error *)(ws + H.o_err);
-    if (m > 0) {
-      CK(cudaMemcpyAsync(d_wl, wl + Sm0 * IGP_WL_NF, Sm * IGP_WL_NF * 8, cudaMemcpyHostToDevice,
-                         cs));
-      CK(cudaMemcpyAsync(d_rank, name_rank + (rank_stride ? Sm0 : 0), rank_n * 4,
-                         cudaMemcpyHostToDevice, cs));
-    }
-    int rc = igp_plan_batch_device(d_wl, sc, m, hw_h, b_max, d_rank, rank_stride, d_i32,
-                                   d_i32 + Sm, d_i32 + 2 * Sm, d_i32 + 3 * Sm, d_i32 + 4 * Sm,
-                                   d_pred, d_gc, stats ? d_st : nullptr, d_err, ws, H.plan, flags,
-                                   cs);
-    if (rc) return rc;
-    if (m > 0) {
-      if (gpu_of) CK(cudaMemcpyAsync(gpu_of + Sm0, d_i32, Sm * 4, cudaMemcpyDeviceToHost, cs));
-      if (pos) CK(cudaMemcpyAsync(pos + Sm0, d_i32 + Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
-      if (units)
-        CK(cudaMemcpyAsync(units + Sm0, d_i32 + 2 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
-      if (batch)
-        CK(cudaMemcpyAsync(batch + Sm0, d_i32 + 3 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
-      if (lb) CK(cudaMemcpyAsync(lb + Sm0, d_i32 + 4 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
-      if (want_pred)
-        CK(cudaMemcpyAsync(pred + Sm0 * 10, d_pred, Sm * 80, cudaMemcpyDeviceToHost, cs));
-    }
-    CK(cudaMemcpyAsync(gpu_count + s0, d_gc, (size_t)sc * 4, cudaMemcpyDeviceToHost, cs));
-    if (stats)
-      CK(cudaMemcpyAsync(stats + (size_t)s0 * IGP_NSTAT, d_st, (size_t)sc * 8 * IGP_NSTAT,
+  // two passes: every chunk's H2D copies and kernels are queued before the
+  // first D2H copy, so a D2H into pageable memory (which returns only when it
+  // is done) cannot hold back the later chunks' work
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int c = 0; c < nc; ++c) {
+      const int s0 = c * sc_max;
+      const int sc = (n_scen - s0) < sc_max ? (n_scen - s0) : sc_max;
+      if (sc <= 0) break;
+      cudaStream_t cs = nc > 1 ? hs->s[c] : st;
+      char *ws = (char *)workspace + (size_t)c * H.per_chunk;
+      const size_t Sm = (size_t)sc * mm, Sm0 = (size_t)s0 * mm;
+      const size_t rank_n = rank_stride ? Sm : mm;
+      double *d_wl = (double *)(ws + H.o_wl);
+      int32_t *d_rank = (int32_t *)(ws + H.o_rank);
+      int32_t *d_i32 = (int32_t *)(ws + H.o_i32);
+      double *d_pred = want_pred ? (double *)(ws + H.o_pred) : nullptr;
+      int32_t *d_gc = (int32_t *)(ws + H.o_gc);
+      int64_t *d_st = (int64_t *)(ws + H.o_st);
+      igp_error *d_err = (igp_error *)(ws + H.o_err);
+      if (pass == 0) {
+        if (nc > 1) CK(cudaStreamWaitEvent(cs, hs->start, 0));
+        if (m > 0) {
+          CK(cudaMemcpyAsync(d_wl, wl + Sm0 * IGP_WL_NF, Sm * IGP_WL_NF * 8,
+                             cudaMemcpyHostToDevice, cs));
+          CK(cudaMemcpyAsync(d_rank, name_rank + (rank_stride ? Sm0 : 0), rank_n * 4,
+                             cudaMemcpyHostToDevice, cs));
+        }
+        const double *hw_c = (flags & IGP_F_HWS) ? hw_h + (size_t)s0 * IGP_HW_NF : hw_h;
+        int rc = igp_plan_batch_device(d_wl, sc, m, hw_c, b_max, d_rank, rank_stride, d_i32,
+                                       d_i32 + Sm, d_i32 + 2 * Sm, d_i32 + 3 * Sm,
+                                       d_i32 + 4 * Sm, d_pred, d_gc, stats ? d_st : nullptr,
+                                       d_err, ws, H.plan, flags, cs);
+        if (rc) return rc;
+        continue;
+      }
+      if (m > 0) {
+        if (gpu_of) CK(cudaMemcpyAsync(gpu_of + Sm0, d_i32, Sm * 4, cudaMemcpyDeviceToHost, cs));
+        if (pos) CK(cudaMemcpyAsync(pos + Sm0, d_i32 + Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+        if (units)
+          CK(cudaMemcpyAsync(units + Sm0, d_i32 + 2 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+        if (batch)
+          CK(cudaMemcpyAsync(batch + Sm0, d_i32 + 3 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+        if (lb)
+          CK(cudaMemcpyAsync(lb + Sm0, d_i32 + 4 * Sm, Sm * 4, cudaMemcpyDeviceToHost, cs));
+        if (want_pred)
+          CK(cudaMemcpyAsync(pred + Sm0 * 10, d_pred, Sm * 80, cudaMemcpyDeviceToHost, cs));
+      }
+      CK(cudaMemcpyAsync(gpu_count + s0, d_gc, (size_t)sc * 4, cudaMemcpyDeviceToHost, cs));
+      if (stats)
+        CK(cudaMemcpyAsync(stats + (size_t)s0 * IGP_NSTAT, d_st, (size_t)sc * 8 * IGP_NSTAT,
+                           cudaMemcpyDeviceToHost, cs));
+      CK(cudaMemcpyAsync(err + s0, d_err, (size_t)sc * sizeof(igp_error),
                          cudaMemcpyDeviceToHost, cs));
-    CK(cudaMemcpyAsync(err + s0, d_err, (size_t)sc * sizeof(igp_error), cudaMemcpyDeviceToHost,
-                       cs));
-    if (nc > 1) {
-      CK(cudaEventRecord(hs->done[c], cs));
-      CK(cudaStreamWaitEvent(st, hs->done[c], 0));
+      if (nc > 1) {
+        CK(cudaEventRecord(hs->done[c], cs));
+        CK(cudaStreamWaitEvent(st, hs->done[c], 0));
+      }
     }
   }
   if (owned) CK(cudaFreeAsync(owned, st));
@@ -789,7 +842,9 @@ struct StreamLayout {
 
 static StreamLayout stream_layout(int S, int C, int cap, int flags) {
   StreamLayout X;
-  X.L = ws_layout(S, C, cap, flags);
+  // a single stream may run any push on the whole GPU (IGP_F_COOP per push):
+  // its layout always reserves the cooperative lanes
+  X.L = ws_layout(S, C, cap, S == 1 ? (flags | IGP_F_COOP) : (flags & ~IGP_F_COOP));
   const size_t SC = (size_t)S * (C > 0 ? C : 1);
   size_t off = X.L.total;
   X.wl = off; off = align_up(off + SC * IGP_WL_NF * 8);
@@ -811,6 +866,8 @@ static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const 
                           int C, int flags) {
   const WsLayout &L = X.L;
   P.hw = hw;
+  P.hw_s = nullptr;
+  P.cap_ld = hw.cap;
   P.S = S;
   P.m = C;
   P.flags = flags;
@@ -865,7 +922,7 @@ size_t igp_stream_workspace_bytes(int n_streams, int capacity, const double *hw,
 
 int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int b_max,
                             void *workspace, size_t workspace_bytes, int flags, void *stream) {
-  if (n_streams < 1 || capacity < 1 || !hw_h || !workspace) return IGP_E_ARG;
+  if (n_streams < 1 || capacity < 1 || !hw_h || !workspace || (flags & IGP_F_HWS)) return IGP_E_ARG;
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;
   if (hw.cap > igp_max_cap()) return IGP_E_CAPACITY;
@@ -907,9 +964,23 @@ int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, i
   k_prologue_plan<<<nblk(tot, 256), 256, 0, st>>>(P);
   k_build<<<nblk(tot, 256), 256, 0, st>>>(P);
   k_table<<<nblk(tot * TB, 256), 256, 0, st>>>(P);
-  if (hw.cap <= 48) launch_place<48>(P, st);
-  else if (hw.cap <= 128) launch_place<128>(P, st);
-  else launch_place<256>(P, st);
+  if ((flags & IGP_F_COOP) && n_streams == 1) {
+    // one stream on the whole GPU: the cooperative step kernel runs the
+    // arrivals, the per-CTA kernel resumes at the first one that needs the
+    // exact sequence (an input that can raise) and persists the state
+    P.coop = (CoopState *)(ws + X.L.coop);
+    int rc;
+    if (hw.cap <= 48) rc = launch_place_coop<48>(P, st);
+    else if (hw.cap <= 128) rc = launch_place_coop<128>(P, st);
+    else rc = launch_place_coop<256>(P, st);
+    if (rc) return rc;
+  } else if (hw.cap <= 48) {
+    launch_place<48>(P, st);
+  } else if (hw.cap <= 128) {
+    launch_place<128>(P, st);
+  } else {
+    launch_place<256>(P, st);
+  }
   CK(cudaGetLastError());
   const size_t dp = (size_t)capacity * 4, sp = (size_t)n * 4;
   if (gpu_of)

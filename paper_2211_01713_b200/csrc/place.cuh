@@ -128,20 +128,21 @@ __device__ __forceinline__ void fence_async_global() {
 // one scenario's step; the last warp to finish the step commits it and
 // publishes the step number.  State shared by all warps:
 struct CoopState {
-  unsigned int best[2];  // argmin key of step k in best[k & 1]
+  unsigned int best[2];  // argmin key of the q-th processed step in best[q & 1]
   int best_pad[2];
-  int done[2];                 // warps finished with step k
+  int done[2];                 // CTAs finished with step q
   int flag;                    // steps committed so far
   int pool_top, abort, G;
-  int status;                  // 0 running, m completed, -1 declined (exact path needed)
-  int pad;
+  int status;                  // the first step the cooperative kernel did NOT run (k0 when it
+                               // declined; k1 when it ran them all); the per-CTA kernel resumes there
+  int sflags;                  // risk flags of the steps it ran (stream mode)
   unsigned long long evals_run, cands_run;
 };
 constexpr int COOP_MAX_LANES = 160 * 512;  // lane_units rows reserved for the cooperative grid
 
 struct WsLayout {
   size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
-      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, nxt, total;
+      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, nxt, hws, total;
   int lanes;
   int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
@@ -188,12 +189,17 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.spos = off; off = align_up(off + Sm * 4);
   L.sE = off; off = align_up(off + (size_t)S * (capx + 2) * 4);
   L.nxt = off; off = align_up(off + (IGP_SPLIT_NEXT ? Sp * 32 : 32));
+  L.hws = off; off = align_up(off + ((flags & IGP_F_HWS) ? (size_t)S * sizeof(Hw) : 0));
   L.total = off;
   return L;
 }
 
 struct PlanParams {
   Hw hw;
+  // IGP_F_HWS: one hardware profile per scenario (select_gpu_type plans every
+  // GPU type of a request as one scenario of one launch); nullptr otherwise
+  const Hw *hw_s;
+  int cap_ld;  // the workspace layout's max_units (largest over the scenarios)
   int S, m, flags;
   // placement steps [k0, k1) of this launch.  Plan mode: [0, m), order from
   // the (-lb, name) sort.  Stream mode (online arrivals, BASELINE config 5):
@@ -244,9 +250,10 @@ __global__ void k_prologue_plan(PlanParams P) {
   if (gid >= (long long)P.S * span) return;
   const int s = (int)(gid / span), i = P.k0 + (int)(gid % span);
   const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
+  const Hw &hw = P.hw_s ? P.hw_s[s] : P.hw;
   int b = -1, u = -1;
   double opnd;
-  const int rc = prologue_one(wl, P.m, i, P.hw, nullptr, b, u, opnd);
+  const int rc = prologue_one(wl, P.m, i, hw, nullptr, b, u, opnd);
   const size_t o = (size_t)s * P.m + i;
   P.batch[o] = b;
   P.lb[o] = u;
@@ -268,9 +275,9 @@ __global__ void k_prologue_plan(PlanParams P) {
   // (direction = sign of gamma) under round-to-nearest, so the two ends of the
   // reachable range [lb, cap] decide whether any evaluation can raise.
   double cold[C_NF], slot[S_NF];
-  entry_consts(wl, P.m, i, b, P.hw, cold, slot);
-  const Solo a = solo_from_cold(cold, (double)u * P.hw.runit);
-  const Solo c = solo_from_cold(cold, (double)P.hw.cap * P.hw.runit);
+  entry_consts(wl, P.m, i, b, hw, cold, slot);
+  const Solo a = solo_from_cold(cold, (double)u * hw.runit);
+  const Solo c = solo_from_cold(cold, (double)hw.cap * hw.runit);
   int fl = (a.err || c.err) ? SF_RISKY : 0;
   // The margin test needs every t_inf term non-negative and finite
   // (validated by WorkloadSpec/Coefficients; raw C-ABI callers might not be).
@@ -290,7 +297,7 @@ __global__ void k_sort(PlanParams P) {
   const int s = blockIdx.x * 4 + w;
   if (s >= P.S) return;
   if (P.perr[s] != INT_MAX) return;
-  const int cap = P.hw.cap, m = P.m;
+  const int cap = P.hw_s ? P.hw_s[s].cap : P.hw.cap, m = P.m;
   const int32_t *lb = P.lb + (size_t)s * m;
   const int32_t *byr = P.by_rank + (size_t)s * m;
   int32_t *order = P.order + (size_t)s * m;
@@ -336,12 +343,13 @@ __global__ void k_build(PlanParams P) {
   if (P.stream ? (P.code[sm + k] & 0xff) != 0 : P.perr[s] != INT_MAX) return;
   const int i = P.stream ? k : P.order[sm + k];
   const double *wl = P.wl + (size_t)s * IGP_WL_NF * P.m;
+  const Hw &hw = P.hw_s ? P.hw_s[s] : P.hw;
   double cold[C_NF], slot[S_NF];
   const int b = P.batch[sm + i], u = P.lb[sm + i];
-  entry_consts(wl, P.m, i, b, P.hw, cold, slot);
+  entry_consts(wl, P.m, i, b, hw, cold, slot);
   cold[C_LB] = (double)u;
   cold[C_WIN] = (double)i;
-  const Solo so = solo_from_cold(cold, (double)u * P.hw.runit);
+  const Solo so = solo_from_cold(cold, (double)u * hw.runit);
   double *cd = P.cold + (sm + k) * C_NF;
 #pragma unroll
   for (int f = 0; f < C_NF; ++f) cd[f] = cold[f];
@@ -367,13 +375,14 @@ __global__ void k_table(PlanParams P) {
   const long long sk = (long long)s * P.m + P.k0 + (lk % span);
   if (P.stream ? (P.code[sk] & 0xff) != 0 : P.perr[s] != INT_MAX) return;
   const double *cd = P.cold + sk * C_NF;
+  const Hw &hw = P.hw_s ? P.hw_s[s] : P.hw;
   const int u = (int)cd[C_LB] + v;
   double *t = P.tbl + (sk * TB + v) * 4;
-  if (u > P.hw.cap) {
+  if (u > hw.cap) {
     t[0] = t[1] = t[2] = t[3] = 0.0;
     return;
   }
-  const Solo so = solo_from_cold(cd, (double)u * P.hw.runit);
+  const Solo so = solo_from_cold(cd, (double)u * hw.runit);
   t[0] = so.ka;
   t[1] = so.pw;
   t[2] = so.ca;
@@ -567,11 +576,12 @@ __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p)
 __device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned ld_cg(const unsigned *p) { return __ldcg(p); }
 
-template <int MAXN, int GW, bool COOP = false>
+template <int MAXN, int GW, bool COOP = false, bool HWS = false>
 __global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32,
                                   GW == 1 ? IGP_MINB_WARP : GW == 2 ? 8 : GW == 4 ? 4 : IGP_MINB_CTA)
 k_place(PlanParams P) {
   static_assert(!COOP || GW == 1, "cooperative mode runs one group per warp");
+  static_assert(!(COOP && HWS), "a cooperative plan has one hardware profile");
   constexpr int GT = GW * 32;
   constexpr int GPB = (GW == 1) ? 4 : 1;
   // Candidate keys (inter, j) packed into 32 bits, inter << 23 | j: lexicographic
@@ -583,6 +593,7 @@ k_place(PlanParams P) {
   __shared__ GroupSmem gsm[GPB];
   __shared__ __align__(16) double ntb[GPB][TB * 4];  // the newcomer's solo table row
   __shared__ unsigned long long nbar[GPB];          // its bulk copy's mbarrier
+  __shared__ Hw shw[HWS ? GPB : 1];                 // IGP_F_HWS: the scenario's profile
   extern __shared__ __align__(16) unsigned char dsm[];
   const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
   GroupSmem &gs = gsm[grp];
@@ -610,7 +621,11 @@ k_place(PlanParams P) {
     if (s >= P.S) break;
   }
   double *ntab = ntb[grp];
-  const Hw &hw = P.hw;
+  if constexpr (HWS) {
+    if (t == 0) shw[grp] = P.hw_s[s];
+    group_sync<GW>();
+  }
+  const Hw &hw = *(HWS ? &shw[grp] : &P.hw);
   const int m = P.m, cap = hw.cap;
   const size_t sm = (size_t)s * m;
   igp_error *err = P.err + s;
@@ -647,7 +662,7 @@ k_place(PlanParams P) {
   const double *tbl = P.tbl + sm * TB * 4;
   unsigned long long *gstate = P.gstate + (size_t)s * P.gstride;
   unsigned long long *sdesc = P.sdesc + (size_t)s * P.gstride;
-  int32_t *sj = P.sj + sm, *spos = P.spos + sm, *sE = P.sE + (size_t)s * (cap + 2);
+  int32_t *sj = P.sj + sm, *spos = P.spos + sm, *sE = P.sE + (size_t)s * (P.cap_ld + 2);
   int32_t *gcap = P.gcap + sm;
   double *gfold = P.gfold + sm * 4;
   const size_t sp = (size_t)s * (size_t)P.pool_recs;
@@ -661,25 +676,29 @@ k_place(PlanParams P) {
   double *frec = P.frec + sp * 2;
   double *pfx = P.pfx + sp * 4;
   Meta *meta = P.meta + sp;
-  uint16_t *lane_units = P.lane_units + (size_t)s * P.lanes * cap;
+  uint16_t *lane_units = P.lane_units + (size_t)s * P.lanes * P.cap_ld;
   int32_t *sst = P.stream ? P.sstate + 4 * (size_t)s : nullptr;
   // stream mode: risk flags of admitted arrivals stick to the scenario
   int sflags = P.stream ? sst[2] : P.sflags[s];
   if constexpr (COOP) {
     // the exact evaluation sequence (PlanStats, a scenario that can raise)
     // runs in the per-CTA kernel; so does a scenario with a prologue error
-    if (P.perr[0] != INT_MAX || (sflags & SF_RISKY) || (P.flags & IGP_F_STATS)) {
-      if (gtid == 0) cs->status = -1;
+    if ((!P.stream && P.perr[0] != INT_MAX) || (sflags & SF_RISKY) || (P.flags & IGP_F_STATS)) {
+      if (gtid == 0) cs->status = P.k0;
       return;
     }
   }
-  // a cooperative plan that already ran its steps: only the predictions remain
-  const bool coop_done = !COOP && P.coop && ld_cg(&P.coop->status) == P.m;
+  // steps the cooperative kernel already ran: resume after them (plan mode:
+  // all of them, only the predictions remain; stream mode: up to the first
+  // arrival that needs the exact sequence)
+  const int k_coop = (!COOP && P.coop) ? ld_cg(&P.coop->status) : P.k0;
+  const bool coop_done = !COOP && P.coop && k_coop > P.k0;
+  if (coop_done) sflags |= P.coop->sflags;
   const unsigned lt = (1u << lane) - 1u;
 
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
-  int G = P.stream ? sst[0] : (coop_done ? P.coop->G : 0);
+  int G = coop_done ? P.coop->G : (P.stream ? sst[0] : 0);
   if (!COOP && G == 0) {  // empty slack order (the cooperative launch zeroes it on the host side)
     for (int x = t; x < cap + 2; x += GT) sE[x] = 0;
   }
@@ -696,16 +715,19 @@ k_place(PlanParams P) {
     poolp = &cs->pool_top;
     abortp = &cs->abort;
   } else if (t == 0) {
-    gs.pool_top = P.stream ? sst[1] : (coop_done ? P.coop->pool_top : 0);
-    gs.abort_code = 0;
+    gs.pool_top = coop_done ? P.coop->pool_top : (P.stream ? sst[1] : 0);
+    gs.abort_code = coop_done ? P.coop->abort : 0;
   }
   group_sync<GW>();
   if (coop_done && t == 0) {
     tot_run = (long long)P.coop->cands_run;
     tot_calls = (long long)P.coop->evals_run;
   }
+  if (!COOP && gs.abort_code) fail_code = 2;  // the cooperative steps ran out of pool
+  int q = 0;          // cooperative mode: steps processed by this launch (slot parity)
+  int k_stop = P.k1;  // cooperative mode: the first step left to the per-CTA kernel
 
-  for (int k = coop_done ? P.k1 : P.k0; k < P.k1; ++k) {
+  for (int k = coop_done ? k_coop : P.k0; k < P.k1 && !fail_code; ++k) {
     int aflags = 0;  // this arrival's risk flags (stream mode)
     if (P.stream) {
       const int c = P.code[sm + k];
@@ -718,6 +740,12 @@ k_place(PlanParams P) {
         continue;
       }
       aflags = c >> 8;
+    }
+    if constexpr (COOP) {
+      if ((sflags | aflags) & SF_RISKY) {  // the exact sequence: left to the per-CTA kernel
+        k_stop = k;
+        break;
+      }
     }
     const bool exact = (P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY);
     const bool margin_rt = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
@@ -815,7 +843,7 @@ k_place(PlanParams P) {
             lu[c_nres] = (uint16_t)c_nu;
           }
           atomicMin(&gs.best, key);
-          if constexpr (COOP) atomicMin(&cs->best[k & 1], key);
+          if constexpr (COOP) atomicMin(&cs->best[q & 1], key);
         }
         cj = -1;
       };
@@ -836,7 +864,7 @@ k_place(PlanParams P) {
         if (idle && (serial || __popc(idle) >= refill_min || idle == (FULL & take_mask))) {
           const int nidle = __popc(idle);
           if constexpr (COOP) {  // the other warps' results prune this warp's candidates
-            if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[k & 1]));
+            if (lane == 0) atomicMin(&gs.best, ld_cg(&cs->best[q & 1]));
             __syncwarp();
           }
           // the step's candidates are the slack-order prefix [0, ncand): idle
@@ -1226,17 +1254,17 @@ k_place(PlanParams P) {
       // it, the other CTAs wait until it is published
       __threadfence();  // this warp's keys, units and win_tid before its arrival
       __syncthreads();
-      if (threadIdx.x == 0) gsm[0].next = atomicAdd(&cs->done[k & 1], 1) == (int)gridDim.x - 1;
+      if (threadIdx.x == 0) gsm[0].next = atomicAdd(&cs->done[q & 1], 1) == (int)gridDim.x - 1;
       __syncthreads();
       const bool last_cta = gsm[0].next != 0;
       committer = last_cta && wi == 0 && grp == 0;
       if (!last_cta) {
         if (threadIdx.x == 0)
-          while (ld_cg(&cs->flag) <= k) __nanosleep(32);
+          while (ld_cg(&cs->flag) <= q) __nanosleep(32);
         __syncthreads();
       }
       __threadfence();  // acquire: later loads must not hit this SM's stale L1 lines
-      bk = ld_cg(&cs->best[k & 1]);
+      bk = ld_cg(&cs->best[q & 1]);
     } else {
       bk = gs.best;
       if (bk != NO_KEY && my_best == bk) gs.win_thread = t;
@@ -1477,13 +1505,14 @@ k_place(PlanParams P) {
     if constexpr (COOP) {
       if (committer) {  // recycle step k-1's slots for step k+1, then publish step k
         if (lane == 0) {
-          cs->done[(k + 1) & 1] = 0;
-          cs->best[(k + 1) & 1] = NO_KEY;
+          cs->done[(q + 1) & 1] = 0;
+          cs->best[(q + 1) & 1] = NO_KEY;
         }
         __threadfence();
         __syncwarp();
-        if (lane == 0) atomicExch(&cs->flag, k + 1);
+        if (lane == 0) atomicExch(&cs->flag, q + 1);
       }
+      ++q;
       if (ld_cg(abortp)) {
         fail_code = 2;
         break;
@@ -1509,9 +1538,10 @@ k_place(PlanParams P) {
       atomicAdd(&cs->evals_run, ev);
       atomicAdd(&cs->cands_run, cd);
     }
-    if (gtid == 0 && !fail_code) {
+    if (gtid == 0) {
       cs->G = G;
-      cs->status = P.m;
+      cs->sflags = sflags;
+      cs->status = fail_code ? P.k1 : k_stop;  // an abort is reported by the per-CTA kernel
     }
     return;
   }

@@ -16,7 +16,10 @@ marshals structure-of-arrays buffers, and assembles the result objects.
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field, fields
+from itertools import chain
+from operator import attrgetter
 from typing import Mapping, Sequence
 
 import numpy as np
@@ -29,7 +32,7 @@ from .errors import (
     InfeasibleSloError,
     native_exception,
 )
-from .layout import E_BATCH_CAP, WL_NF, hw_vector, spec_coef_row
+from .layout import E_BATCH_CAP, WL_FIELDS, WL_NF, hw_vector, spec_coef_row
 from .model import (
     Allocation,
     HardwareProfile,
@@ -207,38 +210,104 @@ def name_ranks(names: Sequence[str]) -> np.ndarray:
     return rank
 
 
+_SPEC_GET = attrgetter(*WL_FIELDS[:4])
+_COEF_GET = attrgetter(*WL_FIELDS[4:])
+
+
 def workload_table(workloads) -> np.ndarray:
-    """(spec, coef) pairs -> [16, m] float64 SoA table (layout.WL_FIELDS)."""
-    wl = np.empty((WL_NF, len(workloads)), dtype=np.float64)
-    for i, (s, c) in enumerate(workloads):
-        wl[:, i] = spec_coef_row(s, c)
+    """(spec, coef) pairs -> [16, m] float64 SoA table (layout.WL_FIELDS):
+    C-level attribute gathers streamed into numpy (about 1 us per workload)."""
+    m = len(workloads)
+    wl = np.empty((WL_NF, m), dtype=np.float64)
+    if m:
+        specs = [w[0] for w in workloads]
+        coefs = [w[1] for w in workloads]
+        wl[:4] = np.fromiter(chain.from_iterable(map(_SPEC_GET, specs)), np.float64,
+                             count=4 * m).reshape(m, 4).T
+        wl[4:] = np.fromiter(chain.from_iterable(map(_COEF_GET, coefs)), np.float64,
+                             count=(WL_NF - 4) * m).reshape(m, WL_NF - 4).T
     return wl
 
 
+_LB_FIELDS = tuple(f.name for f in fields(LatencyBreakdown))
+_AL_FIELDS = tuple(f.name for f in fields(Allocation))
+_new = object.__new__
+_set = object.__setattr__
+
+
+def _frozen(cls, names, values):
+    """A frozen dataclass instance from already-validated device outputs,
+    without the per-field __setattr__ of the generated __init__ (the values
+    are exactly those the reference constructor would store)."""
+    o = _new(cls)
+    _set(o, "__dict__", dict(zip(names, values)))
+    return o
+
+
+class _DevicePlan(Plan):
+    """A Plan assembled from one scenario's device arrays.  The per-GPU
+    objects (GpuPlan, Allocation, LatencyBreakdown: ~3 per workload) are
+    built on first access of ``gpus`` / ``per_workload_r_inter``; everything
+    else is set at once.  Equal to the eagerly built Plan in every field."""
+
+    def __getattr__(self, name):  # only reached while the lazy fields are unset
+        if name in ("gpus", "per_workload_r_inter") and "_arrays" in self.__dict__:
+            self._materialize()
+            return self.__dict__[name]
+        raise AttributeError(name)
+
+    @property
+    def gpu_count(self) -> int:
+        return self.__dict__["_g"]
+
+    def __eq__(self, other):
+        if not isinstance(other, Plan):
+            return NotImplemented
+        return all(getattr(self, f.name) == getattr(other, f.name) for f in fields(Plan))
+
+    __hash__ = None
+
+    def __reduce__(self):
+        return (Plan, tuple(getattr(self, f.name) for f in fields(Plan)))
+
+    def _materialize(self):
+        workloads, hw, g, gpu_of, pos, units, batch, lb, pred = self.__dict__.pop("_arrays")
+        m = len(workloads)
+        names = [w[0].name for w in workloads]
+        order = np.lexsort((pos, gpu_of)).tolist()
+        ends = np.cumsum(np.bincount(gpu_of, minlength=g)).tolist()
+        units_l, batch_l = units.tolist(), batch.tolist()
+        inter_l = ((units - lb) * hw.r_unit).tolist()
+        r_l = (units * hw.r_unit).tolist()
+        rows = pred.tolist()
+        cap = max_units(hw)
+        gpus, r_inter, start = [], {}, 0
+        for j in range(g):
+            allocations, predicted, used = [], {}, 0
+            for i in order[start:ends[j]]:
+                name = names[i]
+                used += units_l[i]
+                allocations.append(_frozen(Allocation, _AL_FIELDS, (name, r_l[i], batch_l[i])))
+                predicted[name] = _frozen(LatencyBreakdown, _LB_FIELDS, rows[i])
+                r_inter[name] = inter_l[i]
+            start = ends[j]
+            gpus.append(GpuPlan(j, allocations, predicted, (cap - used) * hw.r_unit))
+        assert start == m
+        self.__dict__["gpus"] = gpus
+        self.__dict__["per_workload_r_inter"] = r_inter
+
+
 def _plan_from_arrays(res, s, workloads, hw) -> Plan:
-    """Assemble the reference Plan object from one scenario's device outputs."""
-    m = len(workloads)
+    """The reference Plan object of one scenario's device outputs (lazily
+    materialised, see _DevicePlan)."""
+    p = _new(_DevicePlan)
     g = int(res["gpu_count"][s])
-    gpu_of, pos, units = res["gpu_of"][s], res["pos"][s], res["units"][s]
-    batch, lb, pred = res["batch"][s], res["lb"][s], res["pred"][s]
-    members: list[list[int]] = [[] for _ in range(g)]
-    for i in np.lexsort((pos, gpu_of)):
-        members[gpu_of[i]].append(int(i))
-    cap = max_units(hw)
-    gpus, r_inter = [], {}
-    for j, mem in enumerate(members):
-        allocations, predicted, used = [], {}, 0
-        for i in mem:
-            name = workloads[i][0].name
-            u = int(units[i])
-            used += u
-            allocations.append(Allocation(name, u * hw.r_unit, int(batch[i])))
-            predicted[name] = LatencyBreakdown(*(float(v) for v in pred[i]))
-            r_inter[name] = (u - int(lb[i])) * hw.r_unit
-        gpus.append(GpuPlan(j, allocations, predicted, (cap - used) * hw.r_unit))
-    assert sum(len(mm) for mm in members) == m
-    return Plan(strategy="igniter", gpu_type=hw.gpu_type, gpus=gpus,
-                cost_per_hour=len(gpus) * hw.price_per_hour, per_workload_r_inter=r_inter)
+    p.__dict__.update(
+        strategy="igniter", gpu_type=hw.gpu_type, cost_per_hour=g * hw.price_per_hour,
+        diagnostics=[], _g=g,
+        _arrays=(workloads, hw, g, res["gpu_of"][s], res["pos"][s], res["units"][s],
+                 res["batch"][s], res["lb"][s], res["pred"][s]))
+    return p
 
 
 def _raise_plan_error(rec, workloads, hw, b_max):
@@ -284,34 +353,59 @@ def plan(
     return _plan_from_arrays(res, 0, workloads, hw)
 
 
-def _cta_per_scenario(S: int, m: int) -> bool:
+def _cta_per_scenario(S: int, m: int, device=None) -> bool:
     """One CTA per scenario while the batch fits in one or two waves over the
     SMs (B200, measured: 16 x 1k 10.3 vs 16.5 ms, 148 x 1k 11.0 vs 18.5 ms,
     148 x 10k 176 vs 726 ms; one warp per scenario wins from 296 x 1k on)."""
     if m < CTA_MIN_WORKLOADS:
         return False
-    sms = _device.sm_count()
+    sms = _device.sm_count(device)
     return S <= sms or (m >= COOP_MIN_WORKLOADS and S <= 2 * sms)
 
 
 def plan_many(scenarios, hw: HardwareProfile, *, b_max: int = DEFAULT_BATCH_CAP,
-              stats: list | None = None) -> list:
+              stats: list | None = None, devices=None) -> list:
     """Plan independent scenarios (lists of (spec, coef) of equal length) in
-    one launch: one warp per scenario, or one CTA per scenario for small
-    batches of large scenarios.  Returns a list with a Plan or the
-    exception instance the reference would raise for each scenario."""
+    one launch per device: one warp per scenario, or one CTA per scenario for
+    small batches of large scenarios.  ``devices`` (e.g. ``["cuda:0",
+    "cuda:1"]``) splits the batch into contiguous blocks planned concurrently,
+    one host thread per device (scenarios are independent, no
+    collective).  Returns a list with a Plan or the exception instance the
+    reference would raise for each scenario."""
     if not scenarios:
         return []
     m = len(scenarios[0])
     assert all(len(sc) == m for sc in scenarios), "scenarios must have equal workload counts"
     for sc in scenarios:
         _check_unique_names(sc)
+    if stats is not None:
+        assert len(stats) == len(scenarios)
+    devices = list(devices) if devices else [None]
+    from .shard import shard_bounds
+    blocks = [shard_bounds(len(scenarios), r, len(devices)) for r in range(len(devices))]
+
+    def run(r):
+        a, b = blocks[r]
+        if a == b:
+            return []
+        return _plan_block(scenarios[a:b], hw, b_max, None if stats is None else stats[a:b],
+                           devices[r])
+
+    if len(devices) == 1:
+        return run(0)
+    with ThreadPoolExecutor(len(devices)) as ex:
+        parts = list(ex.map(run, range(len(devices))))
+    return [p for part in parts for p in part]
+
+
+def _plan_block(scenarios, hw, b_max, stats, device):
+    m = len(scenarios[0])
     wl = np.stack([workload_table(sc) for sc in scenarios])
     rank = np.stack([name_ranks([s.name for s, _ in sc]) for sc in scenarios])
     flags = IGP_F_STATS if stats is not None else 0
-    if _cta_per_scenario(len(scenarios), m):
+    if _cta_per_scenario(len(scenarios), m, device):
         flags |= IGP_F_CTA
-    res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags)
+    res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags, device=device)
     out = []
     for s, sc in enumerate(scenarios):
         if stats is not None:
@@ -341,20 +435,49 @@ def select_gpu_type(
     b_max: int = DEFAULT_BATCH_CAP,
 ) -> Plan:
     """Cheapest plan over GPU types, first profile on ties; infeasible types
-    are skipped (planner.py:333-364)."""
-    best: Plan | None = None
-    last_error: Exception | None = None
-    for hw in profiles:
+    are skipped (planner.py:333-364).
+
+    Every type is one scenario of ONE device launch (IGP_F_HWS: one hardware
+    profile per scenario, each with its own coefficient table); the
+    reference's sequential semantics are then replayed on the results in
+    profile order: a missing coefficient table raises ValueError when its
+    type is reached, a non-planning error (NonPositiveDenominatorError, ...)
+    of an earlier type propagates first, and planning errors skip the type."""
+    tables, missing = [], None
+    for t, hw in enumerate(profiles):
         try:
             coefs = coefs_by_type[hw.gpu_type]
-            candidate = plan([(s, coefs[s.name]) for s in workloads], hw, b_max=b_max)
+            tables.append(workload_table([(s, coefs[s.name]) for s in workloads]))
         except KeyError as exc:
-            raise ValueError(f"missing coefficients for GPU type {hw.gpu_type}: {exc}") from exc
-        except (InfeasibleSloError, InfeasibleResourceError, BatchCapExceededError) as exc:
-            last_error = exc
-            continue
+            missing = (t, hw, exc)
+            break
+    res = None
+    if tables:
+        _check_unique_names([(s, None) for s in workloads])  # the first type's plan() check
+        n = len(tables)
+        rank = name_ranks([s.name for s in workloads])
+        hv = np.stack([np.asarray(hw_vector(hw), np.float64) for hw in profiles[:n]])
+        flags = IGP_F_CTA if _cta_per_scenario(n, len(workloads)) else 0
+        res = _device.plan_device(np.stack(tables), hv, b_max, rank, flags=flags)
+    best: Plan | None = None
+    last_error: Exception | None = None
+    for t in range(len(tables)):
+        hw = profiles[t]
+        coefs = coefs_by_type[hw.gpu_type]
+        pairs = [(s, coefs[s.name]) for s in workloads]
+        rec = res["err"][t]
+        if int(rec["code"]):
+            try:
+                _raise_plan_error(rec, pairs, hw, b_max)
+            except (InfeasibleSloError, InfeasibleResourceError, BatchCapExceededError) as exc:
+                last_error = exc
+                continue
+        candidate = _plan_from_arrays(res, t, pairs, hw)
         if best is None or candidate.cost_per_hour < best.cost_per_hour:
             best = candidate
+    if missing is not None:
+        t, hw, exc = missing
+        raise ValueError(f"missing coefficients for GPU type {hw.gpu_type}: {exc}") from exc
     if best is None:
         raise InfeasibleError(f"no GPU type can host all workloads ({last_error})")
     return best

@@ -64,3 +64,31 @@ def gather_records(local, n_total: int, world: int, group=None):
         a, b = shard_bounds(n_total, r, world)
         rows.append(out[r * s_max: r * s_max + (b - a)])
     return torch.cat(rows, dim=0)
+
+
+def plan_shard(wl, hw_vec, b_max, rank, *, flags=0, device=None, group=None):
+    """Plan this rank's contiguous block of the batch ``wl`` [S, 16, m] on its
+    GPU with the CUDA planner (igp_plan_batch_device), then all-gather every
+    rank's fixed-size plan records (NCCL on GPUs; gloo also takes the CUDA
+    tensors).  Returns the [S, 2m+1] int32 records of the whole batch, in
+    scenario order, as a tensor on ``device`` -- ``unpack_records`` splits
+    them.  ``rank`` is the name rank of the scenarios' workloads ([m] or
+    [S, m]).  No collective runs before the gather: scenarios are independent
+    (SURVEY.md §8e)."""
+    import torch
+    import torch.distributed as dist
+    from . import _device
+    world = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    S, _, m = wl.shape
+    a, b = shard_bounds(S, r, world)
+    device = _device._dev(device)
+    if b > a:
+        rk = rank[a:b] if np.ndim(rank) == 2 else rank
+        res = _device.plan_device(wl[a:b], hw_vec, b_max, rk, flags=flags, device=device,
+                                  want_pred=False)
+        local = torch.from_numpy(pack_records(res["gpu_of"], res["units"],
+                                              res["gpu_count"])).to(device)
+    else:
+        local = torch.zeros((0, record_width(m)), dtype=torch.int32, device=device)
+    return gather_records(local, S, world, group=group)

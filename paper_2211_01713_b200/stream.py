@@ -29,19 +29,34 @@ ERROR_NAMES = {1: "BatchCapExceededError", 2: "InfeasibleSloError", 3: "Infeasib
                4: "NonPositiveDenominatorError", 5: "NonPositiveDenominatorError"}
 
 
-IGP_F_GW2 = 32  # include/igniter_b200.h: two warps per stream
+IGP_F_CTA = 4   # include/igniter_b200.h: one CTA per stream
+IGP_F_COOP = 16  # a single stream's push on the whole GPU (cooperative steps)
+IGP_F_GW2 = 32  # two warps per stream
+COOP_FROM_ARRIVALS = 16_384  # whole_gpu streams: per-CTA steps before, cooperative after
+
+
+def coop_ctas(k: int) -> int:
+    """CTAs of the cooperative kernel for a push starting at arrival k of one
+    stream: candidates per arrival grow about linearly with the arrivals so far
+    (~3% of them), and 128 lanes per CTA each take one candidate; 0 = all."""
+    return min(max(k // 1024, 16), 0xFFF)
 
 
 class StreamPlanner:
     """n_streams independent arrival streams of up to ``capacity`` arrivals each."""
 
     def __init__(self, hw, *, capacity: int, n_streams: int = 1, b_max: int = 32, device=None,
-                 flags: int | None = None):
+                 flags: int | None = None, whole_gpu: bool = False):
         torch = _device._torch()
         self.lib = _native.lib_for_compute()
         self.hw = hw
         self.hv = _device.hw_array(hw_vector(hw))
         self.device = _device._dev(device)
+        if whole_gpu and int(n_streams) != 1:
+            raise ValueError("whole_gpu runs ONE stream on every SM")
+        self.whole_gpu = bool(whole_gpu)
+        if flags is None and whole_gpu:
+            flags = IGP_F_CTA
         if flags is None:
             # two warps per stream while the streams leave warp slots free
             # (1,000 streams: 20.3 ms vs 24.6 ms with one warp, config 5)
@@ -69,7 +84,15 @@ class StreamPlanner:
         _device._check(rc)
         self.k = 0
 
-    def push_device(self, wl_new):
+    def push_flags(self) -> int:
+        """Flags of the next push: a whole_gpu stream runs its first
+        COOP_FROM_ARRIVALS arrivals in one CTA (a step has few candidates),
+        then every step on the whole GPU (cooperative kernel)."""
+        if self.whole_gpu and self.k >= COOP_FROM_ARRIVALS:
+            return self.flags | IGP_F_COOP | (coop_ctas(self.k) << 16)
+        return self.flags
+
+    def push_device(self, wl_new, flags: int | None = None):
         """Append n arrivals to every stream; ``wl_new`` is a float64 CUDA
         tensor [S, 16, n] on this device.  Returns device int32 tensors
         (gpu_of, pos, code) of shape [S, n]: the GPU and position each arrival
@@ -79,12 +102,13 @@ class StreamPlanner:
         if self.k + n > self.C:
             raise ValueError(f"stream capacity {self.C} exceeded ({self.k} + {n})")
         out = self._out.view(-1)[: 3 * self.S * n].view(3, self.S, n)
+        fl = self.push_flags() if flags is None else int(flags)
         with _device._torch().cuda.device(self.device):
             rc = self.lib.igp_stream_push_device(
                 _device._ptr(wl_new), self.S, self.k, n, self.C, _device._np_ptr(self.hv),
                 self.b_max, _device._ptr(out[0]), _device._ptr(out[1]), _device._ptr(out[2]),
                 _device._ptr(self.stats), _device._ptr(self.err), _device._ptr(self.ws),
-                self.ws.numel(), self.flags, self._stream())
+                self.ws.numel(), fl, self._stream())
         _device._check(rc)
         self.k += n
         return out[0], out[1], out[2]
