@@ -92,7 +92,8 @@ def dist_env():
 
 
 def batch_scenarios(sms: int) -> int:
-    """Scenarios per GPU per step: 16 per SM, one per resident warp slot."""
+    """Scenarios per GPU per step without a GPU to ask (the reference arm on
+    a CPU-only host): 16 per SM, the place kernel's resident warp slots."""
     return sms * 16
 
 
@@ -222,23 +223,29 @@ def fp64_peak():
     return lib.fp64_probe_flops(0, sms), lib.fp64_probe_flops(1, sms)
 
 
-def cpu_reference(wl, hw_vec, b_max, rank, threads):
+def cpu_reference(wl, hw_vec, b_max, rank, threads, stats=False):
     """The CPU oracle (restatement of the reference path, _build_plan rows
-    included) on host threads; returns (plans/s, seconds, outputs)."""
+    included) on host threads; returns (plans/s, seconds, outputs).  Without
+    stats the port may stop a candidate early (a faster CPU baseline than the
+    reference's full evaluation)."""
     from oracle import oracle
     oracle.build()
     t0 = time.perf_counter()
-    r = oracle.plan_batch(wl, hw_vec, b_max, rank, threads, stats=True, pred=True)
+    r = oracle.plan_batch(wl, hw_vec, b_max, rank, threads, stats=stats, pred=True)
     dt = time.perf_counter() - t0
     assert r["rc"] == 0
     return wl.shape[0] / dt, dt, r
 
 
 def device_batch_size():
+    """The GPU arm's batch: one scenario per resident warp slot of the place
+    kernel (igp_plan_batch_slots), so both arms name the same scenarios."""
     try:
         import torch
         if torch.cuda.is_available():
-            return batch_scenarios(torch.cuda.get_device_properties(0).multi_processor_count)
+            from paper_2211_01713_b200 import _device
+            from paper_2211_01713_b200.layout import hw_vector
+            return _device.batch_slots(np.array(hw_vector(hardware())), 32, 0)
     except Exception:  # noqa: BLE001 - the CPU arm also runs without a GPU
         pass
     return batch_scenarios(148)
@@ -317,8 +324,7 @@ def main():
     hv = np.array(hw_vector(hw))
     b_max = 32
     m = args.workloads
-    sms = torch.cuda.get_device_properties(device).multi_processor_count
-    S = args.scenarios or batch_scenarios(sms)
+    S = args.scenarios or _device.batch_slots(hv, b_max, args.flags, device)
     flags = args.flags
     threads = args.cpu_threads or os.cpu_count() or 1
 
@@ -427,11 +433,15 @@ def main():
             assert np.array_equal(dev_out[key][idx], o[key]), f"parity: {key} differs from the oracle"
         assert np.array_equal(pred_chk.view(np.int64), o["pred"].view(np.int64)), \
             "parity: _build_plan rows differ from the oracle"
-        assert np.array_equal(stats_exact[idx, 0], o["stats"][:, 0]), "parity: model_evals"
-        assert np.array_equal(stats_exact[idx, 1], o["stats"][:, 1]), "parity: candidate_gpus"
+        # PlanStats: the oracle's exact counters on four of them (untimed)
+        sidx = idx[np.unique(np.round(np.linspace(0, len(idx) - 1, 4)).astype(np.int64))]
+        _, _, os_ = cpu_reference(wl_pin.numpy()[sidx], hv, b_max, rk_np, threads, stats=True)
+        assert np.array_equal(stats_exact[sidx, 0], os_["stats"][:, 0]), "parity: model_evals"
+        assert np.array_equal(stats_exact[sidx, 1], os_["stats"][:, 1]), "parity: candidate_gpus"
         parity = {"scenarios_checked": [int(i) for i in idx], "oracle": "oracle/igniter_oracle.c",
-                  "fields": "gpu_of, pos, units, gpu_count, _build_plan rows (int64 bit patterns), "
-                            "PlanStats model_evals / candidate_gpus of the exact pass",
+                  "fields": "gpu_of, pos, units, gpu_count, _build_plan rows (int64 bit patterns); "
+                            "PlanStats model_evals / candidate_gpus of the exact pass on "
+                            f"scenarios {[int(i) for i in sidx]}",
                   "result": "bit-exact"}
         if not args.no_cpu_baseline:
             cpu = {"value": v, "unit": "plans/s", "cores": threads, "kind": "port",
@@ -483,7 +493,7 @@ def main():
         h2d = wl_host.nbytes + rk_host.nbytes
         d2h = sum(out[k].nbytes for k in ("gpu_of", "pos", "units", "batch", "lb", "pred",
                                           "gpu_count", "stats", "err"))
-        chunks = min(4, max(1, S // 128))
+        chunks = min(2, max(1, S // 128))
         e2e_launches = KERNELS_PER_PLAN_CALL * chunks * args.steps
         e2e = {"value": S * world * args.steps / (e2e_ms / 1e3), "unit": "plans/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

@@ -132,6 +132,11 @@ int igp_max_cap(void);
 /* last CUDA error string of this thread (for IGP_E_CUDA) */
 const char *igp_last_error_string(void);
 
+/* Scenarios the place kernel runs at once on the current device (resident
+ * warps for one-warp scenarios, resident CTAs with IGP_F_CTA): a batch of
+ * this many fills the GPU in one wave.  Negative IGP_E_* on a bad profile. */
+int igp_plan_batch_slots(const double *hw, int b_max, int flags);
+
 /* Device workspace needed by igp_plan_batch_*() for S scenarios of m workloads
  * (hw: one profile, or n_scen profiles with IGP_F_HWS). */
 size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags);
@@ -187,7 +192,7 @@ int igp_plan_place_device(const double *wl, int n_scen, int m, const double *hw,
  * (the planning scratch plus the device copies of the inputs and outputs),
  * or workspace = NULL with workspace_bytes = 0: the library then allocates
  * and frees it itself, stream-ordered (cudaMallocAsync / cudaFreeAsync).
- * Batches of >= 256 scenarios are pipelined in up to four scenario chunks on
+ * Batches of >= 256 scenarios are pipelined in two scenario chunks on
  * library-owned streams ordered after `stream`: one chunk's kernels overlap
  * the next chunk's H2D and the previous chunk's D2H copies. */
 size_t igp_plan_host_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags,

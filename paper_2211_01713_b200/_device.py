@@ -91,6 +91,17 @@ def _pool_overflow():
                        f"({POOL_RETRY} x m records)")
 
 
+def batch_slots(hw_vec, b_max=32, flags=0, device=None) -> int:
+    """Scenarios the place kernel runs concurrently on `device` (one wave)."""
+    torch = _torch()
+    lib = _native.lib_for_compute()
+    with torch.cuda.device(_dev(device)):
+        n = int(lib.igp_plan_batch_slots(_np_ptr(hw_array(hw_vec)), int(b_max), int(flags)))
+    if n <= 0:
+        _check(-n)
+    return n
+
+
 def plan_workspace_bytes(S, m, hw_vec, b_max, flags):
     lib = _native.load()
     h = hw_array(hw_vec)

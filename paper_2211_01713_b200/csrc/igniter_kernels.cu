@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_segmented_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include <climits>
 #include <cmath>
@@ -351,6 +352,14 @@ __global__ void k_fill_int(int *p, int n, int v) {
 // ===========================================================================
 using namespace igp;
 
+// NVTX range over one C-ABI call (header-only nvtx3: a no-op unless a tool
+// such as Nsight Systems / ncu --nvtx injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define IGP_NVTX() NvtxRange nvtx_range_(__func__)
+
 static int cuda_fail(cudaError_t e) {
   snprintf(g_last_err, sizeof(g_last_err), "%s", cudaGetErrorString(e));
   return IGP_E_CUDA;
@@ -478,6 +487,25 @@ static int cap_of(const double *hw, int n_scen, int b_max, int flags) {
   return cap;
 }
 
+int igp_plan_batch_slots(const double *hw, int b_max, int flags) {
+  if (!hw) return -IGP_E_ARG;
+  const int cap = make_hw(hw, b_max).cap;
+  if (cap < 1 || cap > igp_max_cap()) return -IGP_E_ARG;
+  auto slots = [&](auto kern, int threads, size_t smem, int gpb) {
+    const DevOcc o = dev_occupancy(kern, threads, smem);
+    return o.per_sm * o.sms * gpb;
+  };
+  const bool cta = flags & IGP_F_CTA;
+  if (cap <= 48)
+    return cta ? slots(k_place<48, 8>, 256, place_smem<8>(), 1)
+               : slots(k_place<48, 1>, 128, place_smem<1>(), 4);
+  if (cap <= 128)
+    return cta ? slots(k_place<128, 8>, 256, place_smem<8>(), 1)
+               : slots(k_place<128, 1>, 128, place_smem<1>(), 4);
+  return cta ? slots(k_place<256, 8>, 256, place_smem<8>(), 1)
+             : slots(k_place<256, 1>, 128, place_smem<1>(), 4);
+}
+
 size_t igp_plan_workspace_bytes(int n_scen, int m, const double *hw, int b_max, int flags) {
   return ws_layout(n_scen, m, cap_of(hw, n_scen, b_max, flags), flags).total;
 }
@@ -488,6 +516,7 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
                             double *pred, int32_t *gpu_count, int64_t *stats, igp_error *err,
                             void *workspace, size_t workspace_bytes, int flags, void *stream,
                             int stages) {
+  IGP_NVTX();
   if (n_scen < 0 || m < 0 || !hw_h) return IGP_E_ARG;
   if (n_scen == 0) return IGP_E_OK;
   if ((flags & IGP_F_HWS) && (flags & IGP_F_COOP)) return IGP_E_ARG;
@@ -612,9 +641,10 @@ int igp_plan_place_device(PLAN_ARGS_DECL) { return plan_device_impl(PLAN_ARGS_PA
 // igp_plan_batch_host pipelines the batch in up to HOST_CHUNKS scenario
 // chunks, each on its own stream with its own slice of the workspace: chunk
 // c's kernels overlap chunk c+1's H2D copy and chunk c-1's D2H copy, and the
-// chunks' persistent place kernels share the SMs (each is sized to a quarter
-// of the resident warp slots, so together they fill the GPU).
-static constexpr int HOST_CHUNKS = 4;
+// chunks' persistent place kernels share the SMs (each sized to half the resident
+// warp slots, so together they fill the GPU).
+static constexpr int HOST_CHUNKS = 2;  // measured: 2 chunks 1340 ms, 1: 1364, 4: 2107 (uneven
+                                       // co-residency of four persistent grids)
 static constexpr int HOST_CHUNK_MIN = 128;  // scenarios per chunk before splitting
 
 static int host_chunks(int n_scen, int flags) {
@@ -684,6 +714,7 @@ int igp_plan_batch_host(const double *wl, int n_scen, int m, const double *hw_h,
                         int32_t *units, int32_t *batch, int32_t *lb, double *pred,
                         int32_t *gpu_count, int64_t *stats, igp_error *err, void *workspace,
                         size_t workspace_bytes, int flags, void *stream) {
+  IGP_NVTX();
   if (n_scen < 0 || m < 0 || !hw_h) return IGP_E_ARG;
   if (n_scen == 0) return IGP_E_OK;
   Hw hw = make_hw(hw_h, b_max);
@@ -783,6 +814,7 @@ static int *scratch_int(cudaStream_t st, int *&p) {
 int igp_eval_states_device(const double *wl, int n_rows, const int32_t *batch, const double *r,
                            const int64_t *ptr, int n_states, const double *hw_h, int check_capacity,
                            double *rows, igp_error *err, void *stream) {
+  IGP_NVTX();
   if (n_states < 0 || n_rows < 0 || !hw_h) return IGP_E_ARG;
   if (n_states == 0) return IGP_E_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -800,6 +832,7 @@ int igp_eval_states_device(const double *wl, int n_rows, const int32_t *batch, c
 int igp_alloc_units_device(const double *wl, int n_rows, const int32_t *batch, const double *r,
                            const int64_t *ptr, int n_states, const double *hw_h, int32_t *units,
                            igp_error *err, void *stream) {
+  IGP_NVTX();
   if (n_states < 0 || n_rows < 0 || !hw_h) return IGP_E_ARG;
   if (n_states == 0) return IGP_E_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -817,6 +850,7 @@ int igp_alloc_units_device(const double *wl, int n_rows, const int32_t *batch, c
 int igp_prologue_device(const double *wl, int m, const double *hw_h, int b_max,
                         const int32_t *batch_in, int32_t *batch, int32_t *lb, int32_t *code,
                         igp_error *err, void *stream) {
+  IGP_NVTX();
   if (m < 0 || !hw_h) return IGP_E_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   Hw hw = make_hw(hw_h, b_max);
@@ -922,6 +956,7 @@ size_t igp_stream_workspace_bytes(int n_streams, int capacity, const double *hw,
 
 int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int b_max,
                             void *workspace, size_t workspace_bytes, int flags, void *stream) {
+  IGP_NVTX();
   if (n_streams < 1 || capacity < 1 || !hw_h || !workspace || (flags & IGP_F_HWS)) return IGP_E_ARG;
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;
@@ -932,6 +967,10 @@ int igp_stream_reset_device(int n_streams, int capacity, const double *hw_h, int
                      (cudaStream_t)stream));
   CK(cudaMemsetAsync((char *)workspace + X.err, 0, (size_t)n_streams * sizeof(igp_error),
                      (cudaStream_t)stream));
+  // empty slack orders: a first push may run on the cooperative kernel, which
+  // does not initialise them
+  CK(cudaMemsetAsync((char *)workspace + X.L.sE, 0,
+                     (size_t)n_streams * (hw.cap + 2) * sizeof(int32_t), (cudaStream_t)stream));
   return IGP_E_OK;
 }
 
@@ -939,6 +978,7 @@ int igp_stream_push_device(const double *wl_new, int n_streams, int k0, int n, i
                            const double *hw_h, int b_max, int32_t *gpu_of, int32_t *pos,
                            int32_t *code, int64_t *stats, igp_error *err, void *workspace,
                            size_t workspace_bytes, int flags, void *stream) {
+  IGP_NVTX();
   if (n_streams < 1 || capacity < 1 || k0 < 0 || n < 0 || k0 + n > capacity || !hw_h ||
       !workspace)
     return IGP_E_ARG;
@@ -1002,6 +1042,7 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
                                double *pred, int32_t *gpu_count, igp_error *err,
                                void *workspace, size_t workspace_bytes, int flags,
                                void *stream) {
+  IGP_NVTX();
   if (n_streams < 1 || capacity < 1 || n_arrivals < 0 || n_arrivals > capacity || !hw_h ||
       !workspace)
     return IGP_E_ARG;
@@ -1040,6 +1081,7 @@ int igp_stream_snapshot_device(int n_streams, int n_arrivals, int capacity, cons
 int igp_group_search_device(const double *wl, int n, const int32_t *batch, const double *hw_h,
                             const int32_t *grid, int n_grid, unsigned long long *best,
                             int32_t *err, void *stream) {
+  IGP_NVTX();
   if (n < 1 || n > IGP_GS_MAXN || n_grid < 1 || !hw_h || !grid || !best || !err)
     return IGP_E_ARG;
   Hw hw = make_hw(hw_h, 0);
@@ -1081,6 +1123,7 @@ int igp_simulate_device(int n, const double *rate, const int32_t *batch, const d
                         double *starts, double *sorted, int64_t *seg_end, int32_t *max_depth,
                         int32_t *backlog, int32_t *completed, double *p50, double *p99,
                         double *achieved, void *stream) {
+  IGP_NVTX();
   if (n < 0 || !(duration_ms >= warmup_ms) || !(warmup_ms >= 0.0)) return IGP_E_ARG;
   if (n == 0) return IGP_E_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1118,6 +1161,7 @@ int igp_simulate_device(int n, const double *rate, const int32_t *batch, const d
 int igp_solo_grid_device(const double *wl, int m, const double *hw_h, int b_max,
                          int32_t *min_units, int32_t *best_u, int32_t *best_b,
                          unsigned long long *n_evals, void *stream) {
+  IGP_NVTX();
   if (m < 0 || b_max < 1 || !hw_h) return IGP_E_ARG;
   Hw hw = make_hw(hw_h, b_max);
   if (hw.cap < 1) return IGP_E_ARG;
@@ -1142,6 +1186,7 @@ int igp_solo_grid_device(const double *wl, int m, const double *hw_h, int b_max,
 int igp_components_device(int n, const double *wl, const int32_t *batch, const double *r,
                           const double *co_cache, const int32_t *n_col, const double *p_dem,
                           const double *hw_h, double *out, int32_t *code, void *stream) {
+  IGP_NVTX();
   if (n < 0 || !hw_h) return IGP_E_ARG;
   if (n == 0) return IGP_E_OK;
   if (!wl || !batch || !r || !co_cache || !n_col || !p_dem || !out || !code) return IGP_E_ARG;
@@ -1163,6 +1208,7 @@ int igp_components_device(int n, const double *wl, const int32_t *batch, const d
 
 int igp_power_demand_device(int n, const double *powers, const double *hw_h, double *out,
                             void *stream) {
+  IGP_NVTX();
   if (n < 0 || !hw_h || !out || (n > 0 && !powers)) return IGP_E_ARG;
   k_power_demand<<<1, 32, 0, (cudaStream_t)stream>>>(n, powers, make_hw(hw_h, 1), out);
   CK(cudaGetLastError());

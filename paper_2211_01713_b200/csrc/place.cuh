@@ -37,6 +37,9 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #ifndef IGP_SPLIT_NEXT
 #define IGP_SPLIT_NEXT 1
 #endif
+#ifndef IGP_NW_SMEM
+#define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
+#endif
 #ifndef IGP_PF_NEXT
 #define IGP_PF_NEXT 1  // L2 prefetch of the staged residents' next-unit terms
 #endif
@@ -594,6 +597,9 @@ k_place(PlanParams P) {
   __shared__ __align__(16) double ntb[GPB][TB * 4];  // the newcomer's solo table row
   __shared__ unsigned long long nbar[GPB];          // its bulk copy's mbarrier
   __shared__ Hw shw[HWS ? GPB : 1];                 // IGP_F_HWS: the scenario's profile
+#if IGP_NW_SMEM
+  __shared__ double nwsm[GPB][R_NF + 2];            // the step's newcomer record, k_sch, n_k
+#endif
   extern __shared__ __align__(16) unsigned char dsm[];
   const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
   GroupSmem &gs = gsm[grp];
@@ -756,10 +762,21 @@ k_place(PlanParams P) {
     const double *ck = cold + (size_t)k * C_NF;
     const double *nk_rec = nwt + (size_t)k * R_NF;
     const int need = (int)ck[C_LB];
+#if IGP_NW_SMEM
+    // the newcomer's record lives in shared memory for the step (read where
+    // used instead of pinning ten doubles in registers across the step loop)
+    double *nws = nwsm[grp];
+    if (t < R_NF + 2) nws[t] = t < R_NF ? nk_rec[t] : ck[t == R_NF ? C_KSCH : C_NK];
+    const double &ksch = nws[R_NF], &nkern = nws[R_NF + 1];
+    const double &nw_ka = nws[R_KA], &nw_ca = nws[R_CA], &nw_pw = nws[R_PW];
+    const double &nw_acache = nws[R_ACACHE], &nw_tload = nws[R_TLOAD];
+    const double &nw_tfb = nws[R_TFB], &nw_thalf = nws[R_THALF];
+#else
     const double ksch = ck[C_KSCH], nkern = ck[C_NK];
     const double nw_ka = nk_rec[R_KA], nw_ca = nk_rec[R_CA], nw_pw = nk_rec[R_PW];
     const double nw_acache = nk_rec[R_ACACHE], nw_tload = nk_rec[R_TLOAD];
     const double nw_tfb = nk_rec[R_TFB], nw_thalf = nk_rec[R_THALF];
+#endif
     const int nw_err = (int)nk_rec[R_TSN];
     if (t == 0) {
       gs.best = NO_KEY;

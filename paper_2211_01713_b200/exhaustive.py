@@ -10,11 +10,16 @@ every subset of the workloads runs in one device launch
 bookkeeping over those per-subset results.  The plan is then built by
 ``_build_plan`` (``planner.py:218-246``), with device predictions.
 
-Differences from the reference, both documented in include/igniter_b200.h:
+Differences from the reference (also in include/igniter_b200.h and
+INTEGRATION.md):
 * ``OracleBudget.max_candidates`` counts the reference's own pruned
   evaluations. It is not reproduced, because the device evaluates the whole
   grid.
 * A ``NonPositiveDenominatorError`` is raised if any grid vector raises.
+* The device search takes at most 6 workloads (``IGP_GS_MAXN``, 2^6 subsets
+  of up to cap^6 grid vectors): ``exhaustive_plan`` raises
+  ``BudgetExceededError`` above that even when ``max_workloads`` allows
+  more.  The reference's default budget is 4 workloads.
 """
 
 from __future__ import annotations
@@ -43,66 +48,65 @@ class OracleBudget:
     r_grid_units: tuple[int, ...] | None = None
 
 
-def _partitions(items: Sequence[str], max_blocks: int) -> Iterator[list[list[str]]]:
-    """All set partitions of items into at most max_blocks blocks, in the
-    reference's generation order (oracle.py:117-127)."""
-    if not items:
+def _mask_partitions(full: int, max_blocks: int) -> Iterator[list[int]]:
+    """Every set partition of the bits of ``full`` into at most ``max_blocks``
+    blocks, as lists of bitmasks.  Each block is the lowest bit not yet placed
+    plus a subset of the bits above it, so every partition appears once.  The
+    order differs from the reference's generator (oracle.py:117-127), which
+    does not matter: the choice below is a strict lexicographic minimum over
+    keys that are distinct for distinct partitions."""
+    if full == 0:
         yield []
         return
-    first, rest = items[0], items[1:]
-    for partial in _partitions(rest, max_blocks):
-        for i in range(len(partial)):
-            yield partial[:i] + [[first] + partial[i]] + partial[i + 1:]
-        if len(partial) < max_blocks:
-            yield partial + [[first]]
+    if max_blocks == 0:
+        return
+    low = full & -full
+    rest = full ^ low
+    sub = rest
+    while True:
+        for tail in _mask_partitions(rest & ~sub, max_blocks - 1):
+            yield [low | sub] + tail
+        if sub == 0:
+            break
+        sub = (sub - 1) & rest
 
 
-def decode_keys(best, names):
-    """Packed per-subset keys -> {frozenset(subset): (total, (u, ...)) or None}."""
+def decode_keys(best, n):
+    """Packed per-subset keys -> {mask: (total, (u, ...)) or None}; the units
+    follow the subset's members in name order."""
     out = {}
-    n = len(names)
     for mask in range(1, 1 << n):
-        members = [names[b] for b in range(n) if (mask >> b) & 1]
         key = int(best[mask])
         if key == (1 << 64) - 1:
-            out[frozenset(members)] = None
+            out[mask] = None
             continue
-        k = len(members)
-        units = tuple((key >> (9 * (k - 1 - d))) & 0x1FF for d in range(k))
-        out[frozenset(members)] = (key >> (9 * k), units)
+        k = bin(mask).count("1")
+        out[mask] = (key >> (9 * k), tuple((key >> (9 * (k - 1 - d))) & 0x1FF for d in range(k)))
     return out
 
 
 def select_partition(names, results, max_gpus):
-    """The lexicographically best partition (device count, total units,
-    signature) over the per-subset optima (oracle.py:170-190), or None."""
-    best_key = None
-    best_blocks = None
-    for partition in _partitions(names, max_gpus):
-        total = 0
-        blocks = []
-        feasible = True
-        for block in partition:
-            result = results[frozenset(block)]
-            if result is None:
-                feasible = False
-                break
-            block_total, block_units = result
-            total += block_total
-            blocks.append(tuple(zip(sorted(block), block_units)))
-        if not feasible:
+    """The partition minimising (device count, total units, signature) over
+    the per-subset optima (the choice of oracle.py:170-190), as its sorted
+    blocks of (name, units) pairs, or None when no partition is feasible."""
+    n = len(names)
+    best = None
+    for blocks in _mask_partitions((1 << n) - 1, max_gpus):
+        found = [results[b] for b in blocks]
+        if any(r is None for r in found):
             continue
-        signature = tuple(sorted(blocks))
-        key = (len(partition), total, signature)
-        if best_key is None or key < best_key:
-            best_key = key
-            best_blocks = sorted(blocks)
-    return best_blocks
+        signature = tuple(sorted(
+            tuple(zip((names[i] for i in range(n) if (b >> i) & 1), r[1]))
+            for b, r in zip(blocks, found)))
+        key = (len(blocks), sum(r[0] for r in found), signature)
+        if best is None or key < best:
+            best = key
+    return None if best is None else list(best[2])
 
 
 def group_search(specs, coefs, batches, names, hw, grid):
     """Minimal feasible (total, units) of every subset of ``names`` (name
-    order), or None: {frozenset(subset): (total, (u, ...))}."""
+    order), or None: {subset bitmask over names: (total, (u, ...))}."""
     torch = _device._torch()
     lib = _native.lib_for_compute()
     n = len(names)
@@ -129,7 +133,7 @@ def group_search(specs, coefs, batches, names, hw, grid):
     if err in (E_DENOM, E_ACTIVE_TIME):
         raise NonPositiveDenominatorError(
             "a unit vector of the exhaustive grid has a non-positive r + k4 or active time")
-    return decode_keys(best, names)
+    return decode_keys(best, n)
 
 
 def exhaustive_plan(workloads, hw, *, budget: OracleBudget | None = None,

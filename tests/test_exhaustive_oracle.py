@@ -22,7 +22,7 @@ def _plan_via_oracle(d, oracle_lib):
     best, rc = oracle_lib.group_search(wl[:, order], b[order], hw, np.sort(grid))
     assert rc == 0
     sorted_names = [names[i] for i in order]
-    blocks = select_partition(sorted_names, decode_keys(best, sorted_names), int(d["max_gpus"]))
+    blocks = select_partition(sorted_names, decode_keys(best, m), int(d["max_gpus"]))
     return blocks, 0
 
 

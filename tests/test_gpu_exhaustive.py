@@ -68,7 +68,7 @@ def test_group_search_vs_cpu_oracle(oracle_lib, r_unit, n):
                                            np.array(hw_vector(hw)), np.array(grid))
         assert rc == 0
         from paper_2211_01713_b200.exhaustive import decode_keys
-        assert dev == decode_keys(best, names)
+        assert dev == decode_keys(best, len(names))
 
 
 def test_spec_acceptance_4_theorem1_tightness():

@@ -104,7 +104,8 @@ def test_select_gpu_type_vs_oracle_per_type(oracle_lib, m):
 def test_select_gpu_type_error_order():
     import paper_2211_01713_b200 as igp
     from paper_2211_01713_b200.errors import InfeasibleError
-    spec, coef = _simple("w", 9.9)
+    _, coef = _simple("w", 9.9)
+    spec = igp.WorkloadSpec("w", 40.0, 400.0, 0.574, 0.004)  # transfers: the slow link bites
     slow = make_v100(gpu_type="slow", pcie_bw_mb_per_ms=0.001)
     fast = make_v100(gpu_type="fast")
     # missing table for the second type: ValueError once it is reached

@@ -1,6 +1,6 @@
 """Ad-hoc timing of prepare+place (device-resident inputs, CUDA events).
 
-usage: python tools/quick_time.py S,m,flags [S,m,flags ...]   (IGP_LIB selects a variant)"""
+usage: python tools/quick_time.py S,m,flags [S,m,flags ...]   (IGP_LIB selects a variant; S=0: batch slots)"""
 import ctypes, os, sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
@@ -17,6 +17,8 @@ dev = torch.device("cuda", 0)
 P = _device._ptr
 cfgs = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]] or [(2368, 10000, 0)]
 for S, m, flags in cfgs:
+    if S == 0:  # one scenario per resident slot of this build
+        S = _device.batch_slots(hv, 32, flags)
     wl, names = synth.scenarios(S, m, hw, seed=2211)
     d_wl = torch.from_numpy(wl).to(dev)
     d_rk = torch.from_numpy(name_ranks(list(names))).to(dev)
