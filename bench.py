@@ -237,7 +237,7 @@ def cpu_reference(wl, hw_vec, b_max, rank, threads, stats=False):
     return wl.shape[0] / dt, dt, r
 
 
-def device_batch_size():
+def device_batch_size(m=M_DEFAULT):
     """The GPU arm's batch: one scenario per resident warp slot of the place
     kernel (igp_plan_batch_slots), so both arms name the same scenarios."""
     try:
@@ -245,7 +245,7 @@ def device_batch_size():
         if torch.cuda.is_available():
             from paper_2211_01713_b200 import _device
             from paper_2211_01713_b200.layout import hw_vector
-            return _device.batch_slots(np.array(hw_vector(hardware())), 32, 0)
+            return _device.batch_slots(m, np.array(hw_vector(hardware())), 32, 0)
     except Exception:  # noqa: BLE001 - the CPU arm also runs without a GPU
         pass
     return batch_scenarios(148)
@@ -261,7 +261,7 @@ def run_reference(args, rank, world):
     from paper_2211_01713_b200.planner import name_ranks
     hw = hardware()
     threads = args.cpu_threads or os.cpu_count() or 1
-    S = args.scenarios or device_batch_size()
+    S = args.scenarios or device_batch_size(args.workloads)
     idx = check_indices(S, max(args.check, threads))
     wl, names = synth.scenario_batch(S, args.workloads, hw, seed=args.seed, indices=idx)
     rk = name_ranks(list(names))
@@ -324,7 +324,7 @@ def main():
     hv = np.array(hw_vector(hw))
     b_max = 32
     m = args.workloads
-    S = args.scenarios or _device.batch_slots(hv, b_max, args.flags, device)
+    S = args.scenarios or _device.batch_slots(m, hv, b_max, args.flags, device)
     flags = args.flags
     threads = args.cpu_threads or os.cpu_count() or 1
 

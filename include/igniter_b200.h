@@ -132,10 +132,11 @@ int igp_max_cap(void);
 /* last CUDA error string of this thread (for IGP_E_CUDA) */
 const char *igp_last_error_string(void);
 
-/* Scenarios the place kernel runs at once on the current device (resident
- * warps for one-warp scenarios, resident CTAs with IGP_F_CTA): a batch of
- * this many fills the GPU in one wave.  Negative IGP_E_* on a bad profile. */
-int igp_plan_batch_slots(const double *hw, int b_max, int flags);
+/* Scenarios of m workloads the place kernel runs at once on the current
+ * device (resident warps for one-warp scenarios, resident CTAs with
+ * IGP_F_CTA): a batch of this many fills the GPU in one wave.  Negative
+ * IGP_E_* on a bad profile. */
+int igp_plan_batch_slots(int m, const double *hw, int b_max, int flags);
 
 /* Device workspace needed by igp_plan_batch_*() for S scenarios of m workloads
  * (hw: one profile, or n_scen profiles with IGP_F_HWS). */

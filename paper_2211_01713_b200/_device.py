@@ -91,12 +91,14 @@ def _pool_overflow():
                        f"({POOL_RETRY} x m records)")
 
 
-def batch_slots(hw_vec, b_max=32, flags=0, device=None) -> int:
-    """Scenarios the place kernel runs concurrently on `device` (one wave)."""
+def batch_slots(m, hw_vec, b_max=32, flags=0, device=None) -> int:
+    """Scenarios of m workloads the place kernel runs concurrently on `device`
+    (one wave)."""
     torch = _torch()
     lib = _native.lib_for_compute()
     with torch.cuda.device(_dev(device)):
-        n = int(lib.igp_plan_batch_slots(_np_ptr(hw_array(hw_vec)), int(b_max), int(flags)))
+        n = int(lib.igp_plan_batch_slots(int(m), _np_ptr(hw_array(hw_vec)), int(b_max),
+                                         int(flags)))
     if n <= 0:
         _check(-n)
     return n

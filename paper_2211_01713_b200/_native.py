@@ -81,7 +81,7 @@ PROTOTYPES = {
     "igp_max_cap": (_I, []),
     "igp_last_error_string": (ctypes.c_char_p, []),
     "igp_plan_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I]),
-    "igp_plan_batch_slots": (_I, [_VP, _I, _I]),
+    "igp_plan_batch_slots": (_I, [_I, _VP, _I, _I]),
     "igp_plan_host_workspace_bytes": (_SZ, [_I, _I, _VP, _I, _I, _I, _I]),
     "igp_plan_batch_device": (_I, [_VP, _I, _I, _VP, _I, _VP, _I, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP, _SZ, _I, _VP]),

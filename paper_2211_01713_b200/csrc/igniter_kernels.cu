@@ -374,7 +374,7 @@ static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) 
 
 template <int GW>
 static size_t place_smem() {
-  return (size_t)(GW == 1 ? 128 : GW * 32) * sizeof(LaneSlot);
+  return (size_t)(GW == 1 ? 128 : GW * 32) * lane_smem_bytes();
 }
 
 // Per-device launch facts of one kernel instantiation: the opt-in dynamic
@@ -402,10 +402,15 @@ static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
   return o;
 }
 
-template <int MAXN, int GW, bool HWS = false>
+// one-warp scenarios of at least this many workloads use the 5-CTA build
+#ifndef IGP_MINB5_FROM_M
+#define IGP_MINB5_FROM_M 4000
+#endif
+
+template <int MAXN, int GW, bool HWS = false, int MINB = 0>
 static unsigned place_grid(int S) {
   // persistent launch: at most as many groups as can be co-resident
-  const DevOcc o = dev_occupancy(k_place<MAXN, GW, false, HWS>, GW == 1 ? 128 : GW * 32,
+  const DevOcc o = dev_occupancy(k_place<MAXN, GW, false, HWS, MINB>, GW == 1 ? 128 : GW * 32,
                                  place_smem<GW>());
   const int gpb = (GW == 1) ? 4 : 1;
   const long long want = (S + gpb - 1) / gpb;
@@ -431,6 +436,9 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
     k_place<MAXN, 4><<<place_grid<MAXN, 4>(P.S), 128, place_smem<4>(), st>>>(P);
   } else if (P.flags & IGP_F_GW2) {
     k_place<MAXN, 2><<<place_grid<MAXN, 2>(P.S), 64, place_smem<2>(), st>>>(P);
+  } else if (P.m >= IGP_MINB5_FROM_M && MAXN == 48) {
+    k_place<MAXN, 1, false, false, 5>
+        <<<place_grid<MAXN, 1, false, 5>(P.S), 128, place_smem<1>(), st>>>(P);
   } else {
     k_place<MAXN, 1><<<place_grid<MAXN, 1>(P.S), 128, place_smem<1>(), st>>>(P);
   }
@@ -487,8 +495,8 @@ static int cap_of(const double *hw, int n_scen, int b_max, int flags) {
   return cap;
 }
 
-int igp_plan_batch_slots(const double *hw, int b_max, int flags) {
-  if (!hw) return -IGP_E_ARG;
+int igp_plan_batch_slots(int m, const double *hw, int b_max, int flags) {
+  if (!hw || m < 0) return -IGP_E_ARG;
   const int cap = make_hw(hw, b_max).cap;
   if (cap < 1 || cap > igp_max_cap()) return -IGP_E_ARG;
   auto slots = [&](auto kern, int threads, size_t smem, int gpb) {
@@ -498,7 +506,8 @@ int igp_plan_batch_slots(const double *hw, int b_max, int flags) {
   const bool cta = flags & IGP_F_CTA;
   if (cap <= 48)
     return cta ? slots(k_place<48, 8>, 256, place_smem<8>(), 1)
-               : slots(k_place<48, 1>, 128, place_smem<1>(), 4);
+           : m >= IGP_MINB5_FROM_M ? slots(k_place<48, 1, false, false, 5>, 128, place_smem<1>(), 4)
+                                   : slots(k_place<48, 1>, 128, place_smem<1>(), 4);
   if (cap <= 128)
     return cta ? slots(k_place<128, 8>, 256, place_smem<8>(), 1)
                : slots(k_place<128, 1>, 128, place_smem<1>(), 4);

@@ -37,6 +37,9 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #ifndef IGP_SPLIT_NEXT
 #define IGP_SPLIT_NEXT 1
 #endif
+#ifndef IGP_PF_BATCH
+#define IGP_PF_BATCH 0  // L2 prefetch of the next refill batch's tiles
+#endif
 #ifndef IGP_NW_SMEM
 #define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
 #endif
@@ -89,9 +92,10 @@ struct __align__(16) LaneSlot {
   double hpad[4];
 #endif
   double rec[SLOT][R_NF];  // ... and the first SLOT resident records
-  unsigned long long mbar;
-  unsigned long long pad;
 };
+// the per-lane mbarriers of the slots' bulk copies follow the slot array in
+// dynamic shared memory (8 B each, instead of 16 B of padding per slot)
+constexpr size_t lane_smem_bytes() { return sizeof(LaneSlot) + sizeof(unsigned long long); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -579,9 +583,15 @@ __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p)
 __device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned ld_cg(const unsigned *p) { return __ldcg(p); }
 
-template <int MAXN, int GW, bool COOP = false, bool HWS = false>
+// MINB > 0 overrides the resident-CTA target of the one-warp kernel: 5 CTAs
+// (20 warps/SM, 102 registers) for large plans, where more resident scenarios
+// hide more latency (+6.5% at 10k workloads); the default 4 (128 registers,
+// fewer spills) wins on short plans (1k workloads: 81k vs 76k plans/s).
+template <int MAXN, int GW, bool COOP = false, bool HWS = false, int MINB = 0>
 __global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32,
-                                  GW == 1 ? IGP_MINB_WARP : GW == 2 ? 8 : GW == 4 ? 4 : IGP_MINB_CTA)
+                                  MINB ? MINB
+                                       : GW == 1 ? IGP_MINB_WARP
+                                                 : GW == 2 ? 8 : GW == 4 ? 4 : IGP_MINB_CTA)
 k_place(PlanParams P) {
   static_assert(!COOP || GW == 1, "cooperative mode runs one group per warp");
   static_assert(!(COOP && HWS), "a cooperative plan has one hardware profile");
@@ -604,7 +614,9 @@ k_place(PlanParams P) {
   const int grp = threadIdx.x / GT, t = threadIdx.x % GT, wi = t / 32, lane = t % 32;
   GroupSmem &gs = gsm[grp];
   LaneSlot *const sl = reinterpret_cast<LaneSlot *>(dsm) + threadIdx.x;
-  mbar_init(&sl->mbar);
+  unsigned long long *const lbar =
+      reinterpret_cast<unsigned long long *>(dsm + blockDim.x * sizeof(LaneSlot)) + threadIdx.x;
+  mbar_init(lbar);
   if (t == 0) mbar_init(&nbar[grp]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
@@ -820,6 +832,10 @@ k_place(PlanParams P) {
       const unsigned take_mask = serial ? 1u : FULL;
       int cj = -1, c_nres = 0, c_occ = 0, c_sum = 0, c_i = 0, c_dirty = 0, c_off = 0;
       int c_pend = -1, c_pcode = 0, c_nu = 0;
+#if IGP_PF_BATCH
+      int pf_pos = INT_MAX;          // a next-refill position whose tile to prefetch
+      unsigned long long pf_desc = 0;
+#endif
       unsigned c_sb = 0;  // staged residents already bumped inside this candidate
       bool c_flag = false, c_need = false, c_wait = false;
       double c_C = 0.0, c_f = 0.0, c_inv = 1.0, c_tsn = 0.0;
@@ -936,8 +952,8 @@ k_place(PlanParams P) {
                   const int nst = c_nres < SLOT ? c_nres : SLOT;
                   const uint32_t bytes = (uint32_t)(1 + nst) * (R_NF * 8);
                   fence_async_smem();
-                  mbar_expect_tx(&sl->mbar, bytes);
-                  bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, &sl->mbar);
+                  mbar_expect_tx(lbar, bytes);
+                  bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, lbar);
                   c_wait = true;
 #if IGP_SPLIT_NEXT && IGP_PF_NEXT
                   // the staged residents' next-unit terms, read on their first
@@ -984,6 +1000,15 @@ k_place(PlanParams P) {
             }
           }
           qhead += nidle;
+#if IGP_PF_BATCH
+          // the next refill's candidates: load their descriptors now (used
+          // only after this iteration's tile waits, so the load is not on the
+          // critical path) and prefetch their tiles into L2 below
+          if constexpr (GW == 1 && !COOP && !serial) {
+            pf_pos = qhead + lane;
+            if (pf_pos < ncand) pf_desc = sdesc[pf_pos];
+          }
+#endif
           __syncwarp();
         }
         const unsigned busy = __ballot_sync(FULL, cj >= 0);
@@ -999,9 +1024,22 @@ k_place(PlanParams P) {
         if (cj < 0) continue;
         if (c_need) {
           if (c_wait) {
-            mbar_wait(&sl->mbar, c_phase);
+            mbar_wait(lbar, c_phase);
             c_phase ^= 1u;
             c_wait = false;
+#if IGP_PF_BATCH
+            if constexpr (GW == 1 && !COOP && !serial) {
+              if (pf_pos < ncand) {
+                const int n2 = (int)((pf_desc >> 16) & 0xffffu);
+                const uint32_t b2 = (uint32_t)(1 + (n2 < SLOT ? n2 : SLOT)) * (R_NF * 8);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                 rec + (size_t)((int)(pf_desc >> 32) - 1) * R_NF),
+                             "r"(b2)
+                             : "memory");
+                pf_pos = INT_MAX;
+              }
+            }
+#endif
           }
           if (c_pend >= 0) {
             finish(R_ERROR);

@@ -6,8 +6,15 @@
   C3  100,000 workloads, r_unit 0.01, b <= 128: single-plan latency and the
       full solo candidate grid (100,000 x 128 batches x 100 units)
   C4  4,096 independent 1k-workload scenarios: plans/s
-  C5  online stream: 1,000 streams x 1,000 arrivals (1M arrivals), pushed 100
-      arrivals at a time: arrivals/s
+  C5  online re-provisioning stream as BASELINE defines it: ONE stream of 1M
+      arrivals (C2 generator, seed 5), per-CTA steps for the first 16k
+      arrivals then every step on the whole GPU: arrivals/s, bit-exact on a
+      24,576-arrival oracle prefix (tools/c5_stream.py)
+  C5-tenants  1,000 independent streams x 1,000 arrivals (a tenant batch,
+      not C5): arrivals/s
+  api   plan_many() through the object API (host marshalling + lazily built
+        Plan objects included): plans/s at 148 x 10k
+  select  select_gpu_type over 4 GPU types x 1,000 workloads: one launch
 
 Every number is device time (CUDA events on the launching stream, after
 warm-up) with inputs resident in HBM unless the line says otherwise.  One JSON
@@ -226,6 +233,16 @@ def c4():
 
 
 def c5():
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "c5_stream.py"), "1000000",
+                          "4096", "--check", "24576"], capture_output=True, text=True, check=True)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    d["config"] = "C5"
+    d["workload"] = "one stream of 1M arrivals (C2 generator seed 5), arrival order, pushes of 4096"
+    emit(d)
+
+
+def c5tenants():
     from instances import make_v100
     from paper_2211_01713_b200.stream import StreamPlanner
     hw = make_v100()
@@ -251,27 +268,79 @@ def c5():
         torch.cuda.empty_cache()
     best = min(by_width, key=by_width.get)
     ms = by_width[best]
-    sp = StreamPlanner(hw, capacity=L, n_streams=S, flags={"1 warp": 0, "2 warps": 32, "4 warps": 64}[best])
-    for c in chunks:
-        sp.push_device(c)
-    snap = sp.snapshot()
     from oracle import oracle
     from paper_2211_01713_b200.layout import hw_vector as _hv
     t0 = time.perf_counter()
     oracle.stream(wl[0], np.array(_hv(hw)), 32)
     cpu_s = time.perf_counter() - t0
-    emit(dict(config="C5", cpu_oracle_arrivals_per_s_1core=L / cpu_s,
-              cpu_sample=f"one stream of {L} arrivals on 1 core", workload=f"{S} independent streams x {L} arrivals = {S * L} arrivals, "
-                                    f"pushes of {chunk} arrivals per stream",
+    emit(dict(config="C5-tenants", cpu_oracle_arrivals_per_s_1core=L / cpu_s,
+              workload=f"{S} independent streams x {L} arrivals (a tenant batch, not BASELINE C5), "
+                       f"pushes of {chunk} arrivals per stream",
               ms=ms, arrivals_per_s=S * L / (ms / 1e3), us_per_push=ms * 1e3 / len(chunks),
               group_width=best, ms_by_group_width=by_width,
-              gpus_open=int(snap["gpu_count"].sum()),
-              rejected=int((snap["gpu_of"] < 0).sum()),
               multi_gpu="independent streams shard across ranks (SURVEY §8e option B)"))
 
 
+def api():
+    """plan_many through the object API: (spec, coef) objects in, Plan objects out."""
+    import paper_2211_01713_b200 as igp
+    from instances import make_v100
+    hw = make_v100()
+    S, m = 148, 10_000
+    wl, names = synth.scenario_batch(S, m, hw, seed=2211)
+    scen = []
+    for s_ in range(S):
+        scen.append([(igp.WorkloadSpec(str(names[i]), *map(float, wl[s_, :4, i])),
+                      igp.WorkloadCoefficients(int(wl[s_, 4, i]), *map(float, wl[s_, 5:, i])))
+                     for i in range(m)])
+    igp.plan_many(scen[:8], hw)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plans = igp.plan_many(scen, hw)
+    dt = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    n_alloc = sum(len(g.allocations) for g in plans[0].gpus)
+    mat_ms = (time.perf_counter() - t1) * 1e3
+    t0 = time.perf_counter()
+    tabs = [igp.planner.workload_table(sc) for sc in scen[:16]]
+    marshal_ms = (time.perf_counter() - t0) / 16 * 1e3
+    emit(dict(config="api", workload=f"plan_many({S} scenarios x {m} workloads) via the object API",
+              plans_per_s=S / dt, s=dt, host_marshal_ms_per_10k_plan=marshal_ms,
+              plan_object_materialise_ms_per_10k_plan=mat_ms, allocations_plan0=n_alloc,
+              note="includes workload_table/name ranks per scenario, H2D, kernels, D2H; Plan "
+                   "objects are built lazily on first access of .gpus"))
+    del tabs
+
+
+def select():
+    """select_gpu_type over 4 types in one launch vs one plan() per type."""
+    import paper_2211_01713_b200 as igp
+    from instances import make_v100, random_instance
+    rng = np.random.default_rng(3)
+    base = random_instance(rng, 1000, make_v100())
+    specs = [s for s, _ in base]
+    types = [make_v100(gpu_type="a"), make_v100(gpu_type="b", r_unit=0.01, price_per_hour=2.9),
+             make_v100(gpu_type="c", power_max_w=150.0, price_per_hour=2.5),
+             make_v100(gpu_type="d", r_unit=0.05, price_per_hour=2.2)]
+    coefs = {hw.gpu_type: {s.name: c for s, c in base} for hw in types}
+    igp.select_gpu_type(specs, types, coefs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        best = igp.select_gpu_type(specs, types, coefs)
+    one = (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    for _ in range(5):
+        for hw in types:
+            igp.plan([(s, coefs[hw.gpu_type][s.name]) for s in specs], hw)
+    seq = (time.perf_counter() - t0) / 5
+    emit(dict(config="select", workload="select_gpu_type, 4 GPU types x 1,000 workloads",
+              ms_one_launch=one * 1e3, ms_sequential_plans=seq * 1e3, chosen=best.gpu_type,
+              gpus=best.gpu_count))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+    which = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5", "c5tenants", "api", "select"]
     torch.cuda.set_device(0)
     for w in which:
         globals()[w]()

@@ -18,7 +18,7 @@ P = _device._ptr
 cfgs = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]] or [(2368, 10000, 0)]
 for S, m, flags in cfgs:
     if S == 0:  # one scenario per resident slot of this build
-        S = _device.batch_slots(hv, 32, flags)
+        S = _device.batch_slots(m, hv, 32, flags)
     wl, names = synth.scenarios(S, m, hw, seed=2211)
     d_wl = torch.from_numpy(wl).to(dev)
     d_rk = torch.from_numpy(name_ranks(list(names))).to(dev)
