@@ -118,6 +118,12 @@ enum {
                            shares each step (grid-cooperative launch); falls back
                            on the device to IGP_F_CTA when the exact sequence is
                            needed (IGP_F_STATS, or a scenario that can raise) */
+  IGP_F_WIN = 1 << 28,  /* single scenario (n_scen == 1, max_units <= 128): the
+                           windowed speculative kernel plans steps in windows of 8
+                           (phase A: every newcomer of the window against the
+                           window-start GPUs; phase B: in step order, re-running
+                           only the GPUs earlier steps touched); falls back like
+                           IGP_F_COOP.  Combine with IGP_F_CTA. */
   IGP_F_HWS = 128       /* one hardware profile per scenario: hw points to
                            n_scen x IGP_HW_NF doubles (host) instead of one
                            profile.  select_gpu_type (planner.py:333-364) plans

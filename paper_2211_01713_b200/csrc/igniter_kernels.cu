@@ -139,6 +139,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 }  // namespace igp
 
 #include "place.cuh"
+#include "window.cuh"
 #include "grid.cuh"
 #ifndef IGP_GS_MAXN
 #define IGP_GS_MAXN 6
@@ -478,6 +479,17 @@ static int launch_place_coop(PlanParams P, cudaStream_t st) {
   return IGP_E_OK;
 }
 
+// One scenario in windows of speculative steps (window.cuh), then the per-CTA
+// kernel, which writes the plan (or plans it itself when the windowed kernel
+// declined because the exact sequence is needed).
+template <int MAXN>
+static int launch_place_win(PlanParams P, cudaStream_t st) {
+  CK(cudaMemsetAsync(P.coop, 0, sizeof(CoopState), st));
+  k_place_win<MAXN><<<1, WIN_THREADS, 0, st>>>(P);
+  launch_place<MAXN>(P, st);
+  return IGP_E_OK;
+}
+
 extern "C" {
 
 int igp_abi_version(void) { return IGP_ABI_VERSION; }
@@ -564,7 +576,10 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.stream = 0;
   P.code = nullptr;
   P.sstate = nullptr;
-  P.coop = (flags & IGP_F_COOP) && n_scen == 1 ? (CoopState *)(ws + L.coop) : nullptr;
+  if ((flags & IGP_F_WIN) && (n_scen != 1 || hw.cap > 128 || (flags & (IGP_F_COOP | IGP_F_HWS))))
+    flags &= ~IGP_F_WIN;  // the windowed kernel plans one scenario of max_units <= 128
+  P.coop = (flags & (IGP_F_COOP | IGP_F_WIN)) && n_scen == 1 ? (CoopState *)(ws + L.coop)
+                                                            : nullptr;
   P.win_tid = (int32_t *)(ws + L.win_tid);
   P.sdesc = (unsigned long long *)(ws + L.sdesc);
   P.sj = (int32_t *)(ws + L.sj);
@@ -616,7 +631,10 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
     }
   }
   if (stages & 2) {
-    if (P.coop) {
+    if (P.coop && (flags & IGP_F_WIN)) {
+      const int rc = hw.cap <= 48 ? launch_place_win<48>(P, st) : launch_place_win<128>(P, st);
+      if (rc) return rc;
+    } else if (P.coop) {
       int rc;
       if (hw.cap <= 48) rc = launch_place_coop<48>(P, st);
       else if (hw.cap <= 128) rc = launch_place_coop<128>(P, st);

@@ -168,7 +168,8 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const size_t mm = (size_t)(m > 0 ? m : 1);
   const size_t Sm = (size_t)S * mm;
   const int capx = cap > 0 ? cap : 1;
-  L.lanes = (flags & IGP_F_COOP) ? COOP_MAX_LANES : (flags & IGP_F_CTA) ? 256
+  L.lanes = (flags & IGP_F_COOP) ? COOP_MAX_LANES : (flags & IGP_F_WIN) ? 512
+            : (flags & IGP_F_CTA) ? 256
             : (flags & IGP_F_GW4) ? 128 : (flags & IGP_F_GW2) ? 64 : 32;
   L.pool_recs = (long long)pool_factor(flags) * (long long)mm + 4 * TILE0;
   const size_t Sp = (size_t)S * (size_t)L.pool_recs;
@@ -583,6 +584,260 @@ __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p)
 __device__ __forceinline__ int ld_cg(const int *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned ld_cg(const unsigned *p) { return __ldcg(p); }
 
+// next-unit solo terms of pool record ri (variables nxt / rec in scope)
+#if IGP_SPLIT_NEXT
+#define NEXT_AT(ri) (nxt + (size_t)(ri) * 4)
+#else
+#define NEXT_AT(ri) (rec + (size_t)(ri) * R_NF + R_KA1)
+#endif
+
+// Everything the commit of a step touches in one scenario's state.
+struct ScenState {
+  const double *cold, *tbl;
+  unsigned long long *gstate, *sdesc;
+  int32_t *sj, *spos, *sE, *gcap;
+  double *gfold, *rec, *nxt, *frec, *pfx;
+  Meta *meta;
+  size_t sm;  // scenario offset of the [S][m] outputs
+};
+
+// The commit of step k (planner.py:312-319), run by one warp: open a new GPU
+// at [need] when no candidate fits (bk == NO_KEY), else append the newcomer to
+// GPU j = bk's low bits with the winner's unit vector lu (residents' units,
+// then the newcomer's).  Updates the tile (grown by copying when full), the
+// next-unit terms, the fold stream and prefix fold states, the tile header,
+// the GPU descriptor and fold state, and the slack order.
+__device__ __forceinline__ void commit_step(const PlanParams &P, const Hw &hw, const ScenState &Z,
+                                         int k, int need, unsigned bk, const uint16_t *lu,
+                                         int G, int *poolp, int *abortp, const double *nwv,
+                                         double ksch, double nkern, int lane) {
+  constexpr unsigned NO_KEY = 0xffffffffu;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int cap = hw.cap;
+  const double *cold = Z.cold, *tbl = Z.tbl;
+  unsigned long long *gstate = Z.gstate, *sdesc = Z.sdesc;
+  int32_t *sj = Z.sj, *spos = Z.spos, *sE = Z.sE, *gcap = Z.gcap;
+  double *gfold = Z.gfold, *rec = Z.rec, *frec = Z.frec, *pfx = Z.pfx;
+  Meta *meta = Z.meta;
+  const size_t sm = Z.sm;
+  const double nw_ka = nwv[R_KA], nw_ca = nwv[R_CA], nw_pw = nwv[R_PW];
+  const double nw_acache = nwv[R_ACACHE], nw_tload = nwv[R_TLOAD];
+  const double nw_tfb = nwv[R_TFB], nw_thalf = nwv[R_THALF];
+#if IGP_SPLIT_NEXT
+  double *nxt = Z.nxt;
+#endif
+  if (bk == NO_KEY) {
+    if (lane == 0) {
+      const int off = *poolp + 1;  // records after the header slot
+      if (off + TILE0 > P.pool_recs) {
+        *abortp = IGP_E_CAPACITY;
+      } else {
+        *poolp = off + TILE0;
+        gcap[G] = TILE0;
+        gstate[G] = ((unsigned long long)off << 32) | (unsigned)need | (1u << 16);
+        double *r = rec + (size_t)off * R_NF;
+        r[R_KA] = nw_ka;
+        r[R_CA] = nw_ca;
+        r[R_TSN] = (ksch + delta_sch(hw, 2)) * nkern;
+        r[R_ACACHE] = nw_acache;
+        r[R_TLOAD] = nw_tload;
+        r[R_TFB] = nw_tfb;
+        r[R_THALF] = nw_thalf;
+        r[R_PW] = nw_pw;
+        {
+          const Solo s1 = solo_lookup(tbl, cold, hw, k, need, need + 1);
+          double *nx = NEXT_AT(off);
+          nx[0] = s1.ka;
+          nx[1] = s1.pw;
+          nx[2] = s1.ca;
+          nx[3] = (double)s1.err;
+        }
+        frec[(size_t)off * 2] = nw_pw;
+        frec[(size_t)off * 2 + 1] = nw_ca;
+        double *pp = pfx + (size_t)off * 4;
+        pp[0] = pp[1] = pp[2] = pp[3] = 0.0;
+        meta[off] = Meta{k, (uint16_t)need, (uint16_t)need};
+        Neumaier fp, fc;
+        fp.first(nw_pw);
+        fc.first(nw_ca);
+        double *gf = gfold + (size_t)G * 4;
+        gf[0] = fp.s;
+        gf[1] = fp.c;
+        gf[2] = fc.s;
+        gf[3] = fc.c;
+        TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
+        hd->gf[0] = fp.s;
+        hd->gf[1] = fp.c;
+        hd->gf[2] = fc.s;
+        hd->gf[3] = fc.c;
+        hd->meta[0] = meta[off];
+        if (P.stream) {
+          P.gpu_of[sm + k] = G;
+          P.pos[sm + k] = 0;
+        }
+      }
+    }
+    __syncwarp();
+    if (*(volatile int *)abortp == 0)
+      slack_insert(sj, spos, sdesc, sE, G, gstate[G], cap - need, lane);
+  } else {
+    const int j = (int)(bk & 0x7fffffu);
+    const int nres = (int)((gstate[j] >> 16) & 0xffffu);
+    const int occ_old = (int)(gstate[j] & 0xffffu);
+    const int n = nres + 1;
+    int off = (int)(gstate[j] >> 32);
+    const int tcap = gcap[j];
+    if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
+      int noff = 0;
+      if (lane == 0) {
+        noff = *poolp + 1;  // records after the header slot
+        if (noff + 2 * tcap > P.pool_recs) *abortp = IGP_E_CAPACITY;
+        else *poolp = noff + 2 * tcap;
+      }
+      noff = __shfl_sync(FULL, noff, 0);
+      __syncwarp();
+      if (*(volatile int *)abortp == 0) {
+        for (int r = lane; r < nres; r += 32) {
+#pragma unroll
+          for (int f = 0; f < R_NF; ++f)
+            rec[(size_t)(noff + r) * R_NF + f] = rec[(size_t)(off + r) * R_NF + f];
+#if IGP_SPLIT_NEXT
+#pragma unroll
+          for (int f = 0; f < 4; ++f) NEXT_AT(noff + r)[f] = NEXT_AT(off + r)[f];
+#endif
+          frec[(size_t)(noff + r) * 2] = frec[(size_t)(off + r) * 2];
+          frec[(size_t)(noff + r) * 2 + 1] = frec[(size_t)(off + r) * 2 + 1];
+          meta[noff + r] = meta[off + r];
+        }
+        if (lane == 0) gcap[j] = 2 * tcap;
+        off = noff;
+      }
+      __syncwarp();
+    }
+    if (*(volatile int *)abortp == 0) {
+      const double dnext = delta_sch(hw, n + 1);
+      int part = 0;
+      // fold inputs and meta of resident `lane`, handed to the prefix fold
+      // below by shuffles instead of re-reading them from the pool
+      double f_pw = 0.0, f_ca = 0.0;
+      unsigned long long f_mt = 0ull;
+      for (int r = lane; r < n; r += 32) {
+        const int nu = lu[r];
+        double *rr = rec + (size_t)(off + r) * R_NF;
+        if (r < nres) {
+          Meta mt = meta[off + r];
+          if (nu == (int)mt.u && r < 32) {
+            const double2 fv = *reinterpret_cast<const double2 *>(frec + (size_t)(off + r) * 2);
+            f_pw = fv.x;
+            f_ca = fv.y;
+          }
+          if (nu != (int)mt.u) {
+            const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
+            const Solo s1 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu + 1);
+            rr[R_KA] = so.ka;
+            rr[R_CA] = so.ca;
+            rr[R_PW] = so.pw;
+            double *nx = NEXT_AT(off + r);
+            nx[0] = s1.ka;
+            nx[1] = s1.pw;
+            nx[2] = s1.ca;
+            nx[3] = (double)s1.err;
+            frec[(size_t)(off + r) * 2] = so.pw;
+            frec[(size_t)(off + r) * 2 + 1] = so.ca;
+            mt.u = (uint16_t)nu;
+            meta[off + r] = mt;
+            if (r < 32) {
+              f_pw = so.pw;
+              f_ca = so.ca;
+            }
+          }
+          if (r < 32) f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
+          const double *ce = cold + (size_t)mt.k * C_NF;
+          rr[R_TSN] = (ce[C_KSCH] + dnext) * ce[C_NK];
+        } else {
+          const Solo so = (nu == need) ? Solo{nw_ka, nw_pw, nw_ca, 0}
+                                       : solo_lookup(tbl, cold, hw, k, need, nu);
+          const Solo s1 = solo_lookup(tbl, cold, hw, k, need, nu + 1);
+          rr[R_KA] = so.ka;
+          rr[R_CA] = so.ca;
+          rr[R_PW] = so.pw;
+          double *nx = NEXT_AT(off + r);
+          nx[0] = s1.ka;
+          nx[1] = s1.pw;
+          nx[2] = s1.ca;
+          nx[3] = (double)s1.err;
+          rr[R_TSN] = (ksch + dnext) * nkern;
+          rr[R_ACACHE] = nw_acache;
+          rr[R_TLOAD] = nw_tload;
+          rr[R_TFB] = nw_tfb;
+          rr[R_THALF] = nw_thalf;
+          frec[(size_t)(off + r) * 2] = so.pw;
+          frec[(size_t)(off + r) * 2 + 1] = so.ca;
+          const Meta mt{k, (uint16_t)nu, (uint16_t)need};
+          meta[off + r] = mt;
+          if (r < 32) {
+            f_pw = so.pw;
+            f_ca = so.ca;
+            f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
+          }
+        }
+        part += nu;
+      }
+      part = warp_sum(part);
+      __syncwarp();
+      // prefix fold states of this GPU, in resident order (every lane folds
+      // the shuffled terms identically; lane 0 stores them)
+      Neumaier fp, fc;
+      fp.s = fp.c = fc.s = fc.c = 0.0;
+      for (int r = 0; r < n; ++r) {
+        double pw, ca;
+        if (r < 32) {
+          pw = __shfl_sync(FULL, f_pw, r);
+          ca = __shfl_sync(FULL, f_ca, r);
+        } else {
+          pw = frec[(size_t)(off + r) * 2];
+          ca = frec[(size_t)(off + r) * 2 + 1];
+        }
+        if (lane == 0) {
+          double *pp = pfx + (size_t)(off + r) * 4;
+          pp[0] = fp.s;
+          pp[1] = fp.c;
+          pp[2] = fc.s;
+          pp[3] = fc.c;
+        }
+        fp.add(pw);
+        fc.add(ca);
+      }
+      unsigned long long hmeta[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) hmeta[r] = __shfl_sync(FULL, f_mt, r);
+      if (lane == 0) {
+        gstate[j] = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
+        double *gf = gfold + (size_t)j * 4;
+        gf[0] = fp.s;
+        gf[1] = fp.c;
+        gf[2] = fc.s;
+        gf[3] = fc.c;
+        TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
+        hd->gf[0] = fp.s;
+        hd->gf[1] = fp.c;
+        hd->gf[2] = fc.s;
+        hd->gf[3] = fc.c;
+        for (int r = 0; r < n && r < 4; ++r)
+          *reinterpret_cast<unsigned long long *>(&hd->meta[r]) = hmeta[r];
+        if (P.stream) {
+          P.gpu_of[sm + k] = j;
+          P.pos[sm + k] = nres;
+        }
+      }
+      __syncwarp();
+      slack_move_down(sj, spos, sdesc, sE, j,
+                      ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16),
+                      cap - occ_old, cap - part, lane);
+    }
+  }
+}
+
 // MINB > 0 overrides the resident-CTA target of the one-warp kernel: 5 CTAs
 // (20 warps/SM, 102 registers) for large plans, where more resident scenarios
 // hide more latency (+6.5% at 10k workloads); the default 4 (128 registers,
@@ -687,9 +942,6 @@ k_place(PlanParams P) {
   double *rec = P.rec + sp * R_NF;
 #if IGP_SPLIT_NEXT
   double *nxt = P.nxt + sp * 4;
-#define NEXT_AT(ri) (nxt + (size_t)(ri) * 4)
-#else
-#define NEXT_AT(ri) (rec + (size_t)(ri) * R_NF + R_KA1)
 #endif
   double *frec = P.frec + sp * 2;
   double *pfx = P.pfx + sp * 4;
@@ -1332,218 +1584,24 @@ k_place(PlanParams P) {
 #endif
     // ---- commit (planner.py:312-319), one warp of the group ----
     if (committer) {
-      if (bk == NO_KEY) {
-        if (lane == 0) {
-          const int off = *poolp + 1;  // records after the header slot
-          if (off + TILE0 > P.pool_recs) {
-            *abortp = IGP_E_CAPACITY;
-          } else {
-            *poolp = off + TILE0;
-            gcap[G] = TILE0;
-            gstate[G] = ((unsigned long long)off << 32) | (unsigned)need | (1u << 16);
-            double *r = rec + (size_t)off * R_NF;
-            r[R_KA] = nw_ka;
-            r[R_CA] = nw_ca;
-            r[R_TSN] = (ksch + delta_sch(hw, 2)) * nkern;
-            r[R_ACACHE] = nw_acache;
-            r[R_TLOAD] = nw_tload;
-            r[R_TFB] = nw_tfb;
-            r[R_THALF] = nw_thalf;
-            r[R_PW] = nw_pw;
-            {
-              const Solo s1 = solo_lookup(tbl, cold, hw, k, need, need + 1);
-              double *nx = NEXT_AT(off);
-              nx[0] = s1.ka;
-              nx[1] = s1.pw;
-              nx[2] = s1.ca;
-              nx[3] = (double)s1.err;
-            }
-            frec[(size_t)off * 2] = nw_pw;
-            frec[(size_t)off * 2 + 1] = nw_ca;
-            double *pp = pfx + (size_t)off * 4;
-            pp[0] = pp[1] = pp[2] = pp[3] = 0.0;
-            meta[off] = Meta{k, (uint16_t)need, (uint16_t)need};
-            Neumaier fp, fc;
-            fp.first(nw_pw);
-            fc.first(nw_ca);
-            double *gf = gfold + (size_t)G * 4;
-            gf[0] = fp.s;
-            gf[1] = fp.c;
-            gf[2] = fc.s;
-            gf[3] = fc.c;
-            TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
-            hd->gf[0] = fp.s;
-            hd->gf[1] = fp.c;
-            hd->gf[2] = fc.s;
-            hd->gf[3] = fc.c;
-            hd->meta[0] = meta[off];
-            if (P.stream) {
-              P.gpu_of[sm + k] = G;
-              P.pos[sm + k] = 0;
-            }
-          }
-        }
-        __syncwarp();
-        if (*(volatile int *)abortp == 0)
-          slack_insert(sj, spos, sdesc, sE, G, gstate[G], cap - need, lane);
-      } else {
-        const int j = (int)(bk & 0x7fffffu);
-        const int wt = COOP ? P.win_tid[j] : gs.win_thread;
-        const uint16_t *lu = lane_units + (size_t)wt * cap;
-        const int nres = (int)((gstate[j] >> 16) & 0xffffu);
-        const int occ_old = (int)(gstate[j] & 0xffffu);
-        const int n = nres + 1;
-        int off = (int)(gstate[j] >> 32);
-        const int tcap = gcap[j];
-        if (n > tcap) {  // grow the tile: copy it to a fresh one of twice the size
-          int noff = 0;
-          if (lane == 0) {
-            noff = *poolp + 1;  // records after the header slot
-            if (noff + 2 * tcap > P.pool_recs) *abortp = IGP_E_CAPACITY;
-            else *poolp = noff + 2 * tcap;
-          }
-          noff = __shfl_sync(FULL, noff, 0);
-          __syncwarp();
-          if (*(volatile int *)abortp == 0) {
-            for (int r = lane; r < nres; r += 32) {
-#pragma unroll
-              for (int f = 0; f < R_NF; ++f)
-                rec[(size_t)(noff + r) * R_NF + f] = rec[(size_t)(off + r) * R_NF + f];
-#if IGP_SPLIT_NEXT
-#pragma unroll
-              for (int f = 0; f < 4; ++f) NEXT_AT(noff + r)[f] = NEXT_AT(off + r)[f];
-#endif
-              frec[(size_t)(noff + r) * 2] = frec[(size_t)(off + r) * 2];
-              frec[(size_t)(noff + r) * 2 + 1] = frec[(size_t)(off + r) * 2 + 1];
-              meta[noff + r] = meta[off + r];
-            }
-            if (lane == 0) gcap[j] = 2 * tcap;
-            off = noff;
-          }
-          __syncwarp();
-        }
-        if (*(volatile int *)abortp == 0) {
-          const double dnext = delta_sch(hw, n + 1);
-          int part = 0;
-          // fold inputs and meta of resident `lane`, handed to the prefix fold
-          // below by shuffles instead of re-reading them from the pool
-          double f_pw = 0.0, f_ca = 0.0;
-          unsigned long long f_mt = 0ull;
-          for (int r = lane; r < n; r += 32) {
-            const int nu = lu[r];
-            double *rr = rec + (size_t)(off + r) * R_NF;
-            if (r < nres) {
-              Meta mt = meta[off + r];
-              if (nu == (int)mt.u && r < 32) {
-                const double2 fv = *reinterpret_cast<const double2 *>(frec + (size_t)(off + r) * 2);
-                f_pw = fv.x;
-                f_ca = fv.y;
-              }
-              if (nu != (int)mt.u) {
-                const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
-                const Solo s1 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu + 1);
-                rr[R_KA] = so.ka;
-                rr[R_CA] = so.ca;
-                rr[R_PW] = so.pw;
-                double *nx = NEXT_AT(off + r);
-                nx[0] = s1.ka;
-                nx[1] = s1.pw;
-                nx[2] = s1.ca;
-                nx[3] = (double)s1.err;
-                frec[(size_t)(off + r) * 2] = so.pw;
-                frec[(size_t)(off + r) * 2 + 1] = so.ca;
-                mt.u = (uint16_t)nu;
-                meta[off + r] = mt;
-                if (r < 32) {
-                  f_pw = so.pw;
-                  f_ca = so.ca;
-                }
-              }
-              if (r < 32) f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
-              const double *ce = cold + (size_t)mt.k * C_NF;
-              rr[R_TSN] = (ce[C_KSCH] + dnext) * ce[C_NK];
-            } else {
-              const Solo so = (nu == need) ? Solo{nw_ka, nw_pw, nw_ca, 0}
-                                           : solo_lookup(tbl, cold, hw, k, need, nu);
-              const Solo s1 = solo_lookup(tbl, cold, hw, k, need, nu + 1);
-              rr[R_KA] = so.ka;
-              rr[R_CA] = so.ca;
-              rr[R_PW] = so.pw;
-              double *nx = NEXT_AT(off + r);
-              nx[0] = s1.ka;
-              nx[1] = s1.pw;
-              nx[2] = s1.ca;
-              nx[3] = (double)s1.err;
-              rr[R_TSN] = (ksch + dnext) * nkern;
-              rr[R_ACACHE] = nw_acache;
-              rr[R_TLOAD] = nw_tload;
-              rr[R_TFB] = nw_tfb;
-              rr[R_THALF] = nw_thalf;
-              frec[(size_t)(off + r) * 2] = so.pw;
-              frec[(size_t)(off + r) * 2 + 1] = so.ca;
-              const Meta mt{k, (uint16_t)nu, (uint16_t)need};
-              meta[off + r] = mt;
-              if (r < 32) {
-                f_pw = so.pw;
-                f_ca = so.ca;
-                f_mt = *reinterpret_cast<const unsigned long long *>(&mt);
-              }
-            }
-            part += nu;
-          }
-          part = warp_sum(part);
-          __syncwarp();
-          // prefix fold states of this GPU, in resident order (every lane folds
-          // the shuffled terms identically; lane 0 stores them)
-          Neumaier fp, fc;
-          fp.s = fp.c = fc.s = fc.c = 0.0;
-          for (int r = 0; r < n; ++r) {
-            double pw, ca;
-            if (r < 32) {
-              pw = __shfl_sync(FULL, f_pw, r);
-              ca = __shfl_sync(FULL, f_ca, r);
-            } else {
-              pw = frec[(size_t)(off + r) * 2];
-              ca = frec[(size_t)(off + r) * 2 + 1];
-            }
-            if (lane == 0) {
-              double *pp = pfx + (size_t)(off + r) * 4;
-              pp[0] = fp.s;
-              pp[1] = fp.c;
-              pp[2] = fc.s;
-              pp[3] = fc.c;
-            }
-            fp.add(pw);
-            fc.add(ca);
-          }
-          unsigned long long hmeta[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r) hmeta[r] = __shfl_sync(FULL, f_mt, r);
-          if (lane == 0) {
-            gstate[j] = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
-            double *gf = gfold + (size_t)j * 4;
-            gf[0] = fp.s;
-            gf[1] = fp.c;
-            gf[2] = fc.s;
-            gf[3] = fc.c;
-            TileHeader *hd = reinterpret_cast<TileHeader *>(rec + (size_t)(off - 1) * R_NF);
-            hd->gf[0] = fp.s;
-            hd->gf[1] = fp.c;
-            hd->gf[2] = fc.s;
-            hd->gf[3] = fc.c;
-            for (int r = 0; r < n && r < 4; ++r)
-              *reinterpret_cast<unsigned long long *>(&hd->meta[r]) = hmeta[r];
-            if (P.stream) {
-              P.gpu_of[sm + k] = j;
-              P.pos[sm + k] = nres;
-            }
-          }
-          __syncwarp();
-          slack_move_down(sj, spos, sdesc, sE, j,
-                          ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16),
-                          cap - occ_old, cap - part, lane);
-        }
+      const uint16_t *lu_w = nullptr;
+      if (bk != NO_KEY) {
+        const int wt = COOP ? P.win_tid[(int)(bk & 0x7fffffu)] : gs.win_thread;
+        lu_w = lane_units + (size_t)wt * cap;
       }
+      const ScenState Z{cold, tbl, gstate, sdesc, sj, spos, sE, gcap, gfold, rec,
+#if IGP_SPLIT_NEXT
+                        nxt,
+#else
+                        nullptr,
+#endif
+                        frec, pfx, meta, sm};
+#if IGP_NW_SMEM
+      commit_step(P, hw, Z, k, need, bk, lu_w, G, poolp, abortp, nws, ksch, nkern, lane);
+#else
+      const double nwv[R_NF] = {nw_ka, nw_ca, 0.0, nw_acache, nw_tload, nw_tfb, nw_thalf, nw_pw};
+      commit_step(P, hw, Z, k, need, bk, lu_w, G, poolp, abortp, nwv, ksch, nkern, lane);
+#endif
     }
 #if IGP_TIMING
     if (s == 0 && threadIdx.x == 0 && P.stats) {  // phase cycles of scenario 0, warp 0
