@@ -342,8 +342,8 @@ def main():
     d_gc = torch.empty(S, dtype=torch.int32, device=device)
     d_st = torch.empty((S, 6), dtype=torch.int64, device=device)
     d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
-    ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, b_max, flags | IGP_F_STATS),
-                     dtype=torch.uint8, device=device)
+    ws = torch.empty(max(_device.plan_workspace_bytes(S, m, hv, b_max, fl) for fl in
+                         (flags, flags | IGP_F_STATS)), dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
     P = _device._ptr
     hp = _device._np_ptr(hv)

@@ -124,6 +124,12 @@ enum {
                            window-start GPUs; phase B: in step order, re-running
                            only the GPUs earlier steps touched); falls back like
                            IGP_F_COOP.  Combine with IGP_F_CTA. */
+  IGP_F_FAST = 1 << 29, /* batches of one-warp scenarios: run the certified-margin
+                           kernel first (csrc/fast.cuh: every Alg. 2 decision from
+                           O(1) compact-tile evaluations with an error bound, the
+                           exact evaluation inside the margin; bit-identical plans).
+                           Opt-in: measured slower than the exact kernel on the
+                           latency-bound batch */
   IGP_F_HWS = 128       /* one hardware profile per scenario: hw points to
                            n_scen x IGP_HW_NF doubles (host) instead of one
                            profile.  select_gpu_type (planner.py:333-364) plans

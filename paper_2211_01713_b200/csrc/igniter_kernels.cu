@@ -140,6 +140,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 
 #include "place.cuh"
 #include "window.cuh"
+#include "fast.cuh"
 #include "grid.cuh"
 #ifndef IGP_GS_MAXN
 #define IGP_GS_MAXN 6
@@ -419,8 +420,22 @@ static unsigned place_grid(int S) {
   return (unsigned)(want < cap ? want : cap);
 }
 
+static size_t fast_smem() { return 128 * fast_lane_smem(); }
+
+template <int MAXN>
+static unsigned fast_grid(int S) {
+  const DevOcc o = dev_occupancy(k_place_fast<MAXN>, 128, fast_smem());
+  const long long want = (S + 3) / 4;
+  const long long cap = (long long)o.per_sm * o.sms;
+  return (unsigned)(want < cap ? want : cap);
+}
+
 template <int MAXN>
 static void launch_place(const PlanParams &P, cudaStream_t st) {
+  if (P.hand) {  // the certified-margin fast kernel plans what it can; k_place the rest
+    cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
+    k_place_fast<MAXN><<<fast_grid<MAXN>(P.S), 128, fast_smem(), st>>>(P);
+  }
   cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
   if (P.hw_s) {  // one profile per scenario: one CTA or one warp per scenario
     if (P.flags & IGP_F_CTA)
@@ -516,6 +531,10 @@ int igp_plan_batch_slots(int m, const double *hw, int b_max, int flags) {
     return o.per_sm * o.sms * gpb;
   };
   const bool cta = flags & IGP_F_CTA;
+  if (fast_path(flags))
+    return cap <= 48    ? slots(k_place_fast<48>, 128, fast_smem(), 4)
+           : cap <= 128 ? slots(k_place_fast<128>, 128, fast_smem(), 4)
+                        : slots(k_place_fast<256>, 128, fast_smem(), 4);
   if (cap <= 48)
     return cta ? slots(k_place<48, 8>, 256, place_smem<8>(), 1)
            : m >= IGP_MINB5_FROM_M ? slots(k_place<48, 1, false, false, 5>, 128, place_smem<1>(), 4)
@@ -586,6 +605,18 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.spos = (int32_t *)(ws + L.spos);
   P.sE = (int32_t *)(ws + L.sE);
   P.nxt = (double *)(ws + L.nxt);
+  // the layout (sized with the caller's flags) holds the compact tiles
+  const bool fast = L.total > L.hand && fast_path(flags) && !P.coop;
+  P.crec = fast ? (CRec *)(ws + L.crec) : nullptr;
+  P.cnext = fast ? (CNext *)(ws + L.cnext) : nullptr;
+  P.hand = fast ? (Hand *)(ws + L.hand) : nullptr;
+  // the fast kernel's decision margin; IGP_FAST_DELTA raises it (tests force the
+  // exact fallback with it); it is never lowered below FAST_DELTA
+  P.fast_delta = FAST_DELTA;
+  if (const char *e = getenv("IGP_FAST_DELTA")) {
+    const double d = atof(e);
+    if (d > FAST_DELTA) P.fast_delta = d;
+  }
   P.wl = wl;
   P.rank = name_rank;
   P.rank_stride = rank_stride;
@@ -970,6 +1001,10 @@ static void stream_params(PlanParams &P, const StreamLayout &X, char *ws, const 
   P.spos = (int32_t *)(ws + L.spos);
   P.sE = (int32_t *)(ws + L.sE);
   P.nxt = (double *)(ws + L.nxt);
+  P.crec = nullptr;
+  P.cnext = nullptr;
+  P.hand = nullptr;
+  P.fast_delta = FAST_DELTA;
   P.gpu_count = (int32_t *)(ws + X.gc);
   P.stats = nullptr;
   P.err = (igp_error *)(ws + X.err);

@@ -55,7 +55,7 @@ enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_NF };
 enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_KA1, R_PW1, R_CA1,
        R_ERR1, R_NF };
 #endif
-enum { SF_RISKY = 1, SF_NO_MARGIN = 2 };
+enum { SF_RISKY = 1, SF_NO_MARGIN = 2, SF_NO_FAST = 4 };
 enum { R_FEAS = 0, R_INFEAS = 1, R_PRUNED = 2, R_ERROR = 3 };
 
 struct Meta {
@@ -123,6 +123,34 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t phas
       "r"(phase)
       : "memory");
 }
+// Per-thread 16-byte async copies (LDGSTS) completing on an mbarrier.  A
+// lane's candidate tile is staged this way: cp.async.bulk takes its operands
+// from uniform registers, so 32 lanes with 32 different tiles compile to a
+// 32-trip ELECT/R2UR/UBLKCP loop (13.5% of k_place's instructions and 10% of
+// its stall samples in profiles/r02); LDGSTS issues for all lanes at once.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+// the barrier's (single) arrival fires when this thread's prior cp.asyncs land
+__device__ __forceinline__ void cp_async_arrive(unsigned long long *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// ... or tracked as a per-thread group: cp.async.mbarrier.arrive also takes its
+// barrier address from a uniform register (another per-lane ELECT loop, 9.5%
+// of the fast kernel's instructions), commit/wait_group do not
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+// candidate tile staging: 0 = cp.async.bulk + mbarrier, 1 = LDGSTS + mbarrier,
+// 2 = LDGSTS + commit/wait_group
+#ifndef IGP_TILE_LDGSTS
+#define IGP_TILE_LDGSTS 2
+#endif
 // generic-proxy writes -> later async-proxy (TMA) access of the same memory
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -147,9 +175,40 @@ struct CoopState {
 };
 constexpr int COOP_MAX_LANES = 160 * 512;  // lane_units rows reserved for the cooperative grid
 
+// Compact tiles of the certified-margin fast path (fast.cuh).
+#ifndef IGP_FSLOT
+#define IGP_FSLOT 7
+#endif
+// compact resident records staged per lane (a GPU with more residents takes
+// the exact evaluation); 7 keeps six 128-thread CTAs per SM within shared memory
+constexpr int FSLOT = IGP_FSLOT;
+static_assert(FSLOT >= 1 && FSLOT <= 8, "bump counters: 8 bits per staged resident");
+struct __align__(16) CRec {  // a resident's check terms at its committed units
+  double A, B, ca, beta;
+};
+struct __align__(16) CNext {  // ... one unit up, as values and exact deltas of the sums
+  double A1, B1, dca, dpw;
+};
+struct __align__(16) CHead {  // a GPU's power and cache sums (compact tile header)
+  double P, C;
+};
+struct __align__(16) FastSlot {
+  CHead h;
+  CRec r[FSLOT];
+};
+
+// Hand-off from k_place_fast to k_place (which writes the plan and the
+// _build_plan rows): the step where k_place resumes (k1 = all planned, k0 =
+// declined) and the scenario state after the fast steps.
+struct Hand {
+  int k_done, G, pool_top, abort;
+  unsigned long long evals_run, cands_run, exact_run, pad;
+};
+
 struct WsLayout {
   size_t by_rank, order, cold, nw, tbl, gstate, gcap, gfold, rec, frec, pfx, meta,
-      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, nxt, hws, total;
+      lane_units, sflags, perr, sched, coop, win_tid, sdesc, sj, spos, sE, nxt, hws, crec, cnext,
+      hand, total;
   int lanes;
   int gstride;          // per-scenario stride of gstate (multiple of 4: 16-byte scan loads)
   long long pool_recs;  // records per scenario
@@ -160,6 +219,13 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 static int pool_factor(int flags) {
   const int f = (flags >> 8) & 0xff;
   return f ? f : 7;
+}
+
+// IGP_F_FAST: the certified-margin kernel (fast.cuh) runs before k_place for
+// batches of one-warp scenarios.
+static bool fast_path(int flags) {
+  return (flags & IGP_F_FAST) && !(flags & (IGP_F_STATS | IGP_F_CTA | IGP_F_GW2 | IGP_F_GW4 |
+                                            IGP_F_COOP | IGP_F_WIN | IGP_F_HWS));
 }
 
 static WsLayout ws_layout(int S, int m, int cap, int flags) {
@@ -198,6 +264,10 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   L.sE = off; off = align_up(off + (size_t)S * (capx + 2) * 4);
   L.nxt = off; off = align_up(off + (IGP_SPLIT_NEXT ? Sp * 32 : 32));
   L.hws = off; off = align_up(off + ((flags & IGP_F_HWS) ? (size_t)S * sizeof(Hw) : 0));
+  const bool fast = fast_path(flags);
+  L.crec = off; off = align_up(off + (fast ? Sp * sizeof(CRec) : 0));
+  L.cnext = off; off = align_up(off + (fast ? Sp * sizeof(CNext) : 0));
+  L.hand = off; off = align_up(off + (fast ? (size_t)S * sizeof(Hand) : 0));
   L.total = off;
   return L;
 }
@@ -246,6 +316,11 @@ struct PlanParams {
   double *pred;
   int64_t *stats;
   igp_error *err;
+  // certified-margin fast path (fast.cuh); hand == nullptr: not used
+  CRec *crec;
+  CNext *cnext;
+  Hand *hand;
+  double fast_delta;  // decision margin relative to beta (FAST_DELTA; IGP_FAST_DELTA overrides)
 };
 
 // ---------------------------------------------------------------------------
@@ -293,6 +368,8 @@ __global__ void k_prologue_plan(PlanParams P) {
       !(cold[C_NK] >= 0.0) || !(slot[S_ACACHE] >= 0.0) || !(slot[S_ACACHE] <= 1e6) ||
       !isfinite(slot[S_TLOAD] + slot[S_TFB] + slot[S_THALF] + cold[C_KSCH] * cold[C_NK]))
     fl |= SF_NO_MARGIN;
+  // the fast kernel's error bound assumes alpha_cache <= FAST_MAX_ACACHE (fast.cuh)
+  if (!(slot[S_ACACHE] <= 16.0)) fl |= SF_NO_FAST;
   if (!(u <= 0xffff)) fl |= SF_RISKY;
   if (P.stream) P.code[o] = fl << 8;
   else if (fl) atomicOr(&P.sflags[s], fl);
@@ -875,7 +952,9 @@ k_place(PlanParams P) {
   if (t == 0) mbar_init(&nbar[grp]);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+#if IGP_TILE_LDGSTS < 2
   uint32_t c_phase = 0;  // parity of this lane's mbarrier
+#endif
   uint32_t n_phase = 0;  // parity of the group's newcomer-row mbarrier
   CoopState *const cs = P.coop;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;      // cooperative lane id
@@ -961,14 +1040,20 @@ k_place(PlanParams P) {
   // steps the cooperative kernel already ran: resume after them (plan mode:
   // all of them, only the predictions remain; stream mode: up to the first
   // arrival that needs the exact sequence)
-  const int k_coop = (!COOP && P.coop) ? ld_cg(&P.coop->status) : P.k0;
+  int k_coop = (!COOP && P.coop) ? ld_cg(&P.coop->status) : P.k0;
   const bool coop_done = !COOP && P.coop && k_coop > P.k0;
   if (coop_done) sflags |= P.coop->sflags;
+  // steps the certified-margin fast kernel ran (fast.cuh): plan mode, all of
+  // them or none; the predictions and outputs below remain
+  const Hand *const hdp = (!COOP && P.hand) ? P.hand + s : nullptr;
+  const bool fast_done = hdp && !coop_done && hdp->k_done > P.k0;
+  if (fast_done) k_coop = hdp->k_done;
+  const bool resumed = coop_done || fast_done;
   const unsigned lt = (1u << lane) - 1u;
 
   LaneArrays<MAXN> L;
   ModMask<MAXN> mod;
-  int G = coop_done ? P.coop->G : (P.stream ? sst[0] : 0);
+  int G = coop_done ? P.coop->G : fast_done ? hdp->G : (P.stream ? sst[0] : 0);
   if (!COOP && G == 0) {  // empty slack order (the cooperative launch zeroes it on the host side)
     for (int x = t; x < cap + 2; x += GT) sE[x] = 0;
   }
@@ -985,19 +1070,21 @@ k_place(PlanParams P) {
     poolp = &cs->pool_top;
     abortp = &cs->abort;
   } else if (t == 0) {
-    gs.pool_top = coop_done ? P.coop->pool_top : (P.stream ? sst[1] : 0);
-    gs.abort_code = coop_done ? P.coop->abort : 0;
+    gs.pool_top = coop_done ? P.coop->pool_top
+                  : fast_done ? hdp->pool_top
+                              : (P.stream ? sst[1] : 0);
+    gs.abort_code = coop_done ? P.coop->abort : fast_done ? hdp->abort : 0;
   }
   group_sync<GW>();
-  if (coop_done && t == 0) {
-    tot_run = (long long)P.coop->cands_run;
-    tot_calls = (long long)P.coop->evals_run;
+  if (resumed && t == 0) {
+    tot_run = (long long)(coop_done ? P.coop->cands_run : hdp->cands_run);
+    tot_calls = (long long)(coop_done ? P.coop->evals_run : hdp->evals_run);
   }
-  if (!COOP && gs.abort_code) fail_code = 2;  // the cooperative steps ran out of pool
+  if (!COOP && gs.abort_code) fail_code = 2;  // the cooperative / fast steps ran out of pool
   int q = 0;          // cooperative mode: steps processed by this launch (slot parity)
   int k_stop = P.k1;  // cooperative mode: the first step left to the per-CTA kernel
 
-  for (int k = coop_done ? k_coop : P.k0; k < P.k1 && !fail_code; ++k) {
+  for (int k = resumed ? k_coop : P.k0; k < P.k1 && !fail_code; ++k) {
     int aflags = 0;  // this arrival's risk flags (stream mode)
     if (P.stream) {
       const int c = P.code[sm + k];
@@ -1202,10 +1289,27 @@ k_place(PlanParams P) {
                 st_run += 1;
                 {  // stage the tile header and the first SLOT records: one bulk copy
                   const int nst = c_nres < SLOT ? c_nres : SLOT;
+#if IGP_TILE_LDGSTS
+                  {
+                    const char *src = reinterpret_cast<const char *>(rec + (size_t)(c_off - 1) * R_NF);
+                    char *dst = reinterpret_cast<char *>(sl->gf);
+                    constexpr int CPR = R_NF * 8 / 16;  // 16-byte chunks per record
+                    const int nch = (1 + nst) * CPR;
+#pragma unroll
+                    for (int c = 0; c < (1 + SLOT) * CPR; ++c)
+                      if (c < nch) cp_async16(dst + 16 * c, src + 16 * c);
+#if IGP_TILE_LDGSTS == 2
+                    cp_async_commit();
+#else
+                    cp_async_arrive(lbar);
+#endif
+                  }
+#else
                   const uint32_t bytes = (uint32_t)(1 + nst) * (R_NF * 8);
                   fence_async_smem();
                   mbar_expect_tx(lbar, bytes);
                   bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, lbar);
+#endif
                   c_wait = true;
 #if IGP_SPLIT_NEXT && IGP_PF_NEXT
                   // the staged residents' next-unit terms, read on their first
@@ -1276,8 +1380,12 @@ k_place(PlanParams P) {
         if (cj < 0) continue;
         if (c_need) {
           if (c_wait) {
+#if IGP_TILE_LDGSTS == 2
+            cp_async_wait_all();
+#else
             mbar_wait(lbar, c_phase);
             c_phase ^= 1u;
+#endif
             c_wait = false;
 #if IGP_PF_BATCH
             if constexpr (GW == 1 && !COOP && !serial) {
@@ -1674,7 +1782,10 @@ k_place(PlanParams P) {
     P.stats[IGP_NSTAT * s + 1] = st_ok ? (long long)gs.tot[2] : -1;
     P.stats[IGP_NSTAT * s + 2] = st_ok ? (long long)gs.tot[1] : -1;
     P.stats[IGP_NSTAT * s + 3] = (long long)gs.tot[1];
-    P.stats[IGP_NSTAT * s + 4] = st_ok ? (long long)gs.tot[3] : -1;
+    // resident reads (exact mode); with the fast kernel: the candidates it
+    // re-ran with the exact evaluation (decisions inside its margin)
+    P.stats[IGP_NSTAT * s + 4] = st_ok ? (long long)gs.tot[3]
+                                       : fast_done ? (long long)hdp->exact_run : -1;
     P.stats[IGP_NSTAT * s + 5] = (long long)gs.tot[4];
   }
 

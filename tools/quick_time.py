@@ -41,6 +41,7 @@ for S, m, flags in cfgs:
     stats = d_st.cpu().numpy()
     print(f"[{os.path.basename(_native.LIB_PATH)}] S={S} m={m} fl={flags}: place {place:.1f} ms prep {prep:.1f} ms "
           f"-> {S/((place+prep)/1e3):.1f} plans/s; evals_run/scen={stats[:,3].mean():.0f} "
+          f"cands_run/scen={stats[:,5].mean():.0f} exact_fallback/scen={stats[:,4].mean():.1f} "
           f"gpus={d_gc[:3].tolist()} err={np.unique(d_err.cpu().numpy().view(_native.err_dtype())['code'])}", flush=True)
     del ws, d_wl, i32
     torch.cuda.empty_cache()
