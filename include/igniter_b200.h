@@ -110,6 +110,11 @@ enum {
   IGP_F_STATS = 1,      /* exact PlanStats (model_evals, candidate_gpus) for every
                            scenario: no overflow early exit, no bound prune */
   IGP_F_NO_PRED = 2,    /* skip the _build_plan breakdown rows */
+  IGP_F_SMEM = 8,       /* with IGP_F_CTA: one CTA per scenario keeps the search
+                           state in shared memory and evaluates each candidate
+                           with one warp (csrc/smem_plan.cuh; up to about 1,900
+                           workloads, larger scenarios use the per-CTA kernel);
+                           falls back on the device like IGP_F_COOP */
   IGP_F_CTA = 4,        /* one CTA (many warps) per scenario instead of one warp:
                            lower latency for single large plans */
   IGP_F_GW2 = 32,       /* two / four warps per scenario (between the default one */

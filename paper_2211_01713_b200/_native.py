@@ -21,6 +21,7 @@ DEPS = SOURCES + [os.path.join(PKG, "csrc", "exact_fp64.cuh"), os.path.join(PKG,
                   os.path.join(PKG, "csrc", "grid.cuh"), os.path.join(PKG, "csrc", "exhaustive.cuh"),
                   os.path.join(PKG, "csrc", "simulate.cuh"), os.path.join(PKG, "csrc", "components.cuh"),
                   os.path.join(PKG, "csrc", "window.cuh"), os.path.join(PKG, "csrc", "fast.cuh"),
+                  os.path.join(PKG, "csrc", "smem_plan.cuh"),
                   os.path.join(REPO, "include", "igniter_b200.h")]
 
 NVCC_FLAGS = [

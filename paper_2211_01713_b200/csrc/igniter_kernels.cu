@@ -141,6 +141,7 @@ __device__ __forceinline__ void entry_consts(const double *wl, long long ld, int
 #include "place.cuh"
 #include "window.cuh"
 #include "fast.cuh"
+#include "smem_plan.cuh"
 #include "grid.cuh"
 #ifndef IGP_GS_MAXN
 #define IGP_GS_MAXN 6
@@ -408,6 +409,9 @@ static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
 #ifndef IGP_MINB5_FROM_M
 #define IGP_MINB5_FROM_M 4000
 #endif
+#ifndef IGP_MINB_BIG
+#define IGP_MINB_BIG 5  // resident CTAs per SM of the large-plan one-warp build
+#endif
 
 template <int MAXN, int GW, bool HWS = false, int MINB = 0>
 static unsigned place_grid(int S) {
@@ -432,7 +436,7 @@ static unsigned fast_grid(int S) {
 
 template <int MAXN>
 static void launch_place(const PlanParams &P, cudaStream_t st) {
-  if (P.hand) {  // the certified-margin fast kernel plans what it can; k_place the rest
+  if (P.crec) {  // the certified-margin fast kernel plans what it can; k_place the rest
     cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
     k_place_fast<MAXN><<<fast_grid<MAXN>(P.S), 128, fast_smem(), st>>>(P);
   }
@@ -453,8 +457,8 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
   } else if (P.flags & IGP_F_GW2) {
     k_place<MAXN, 2><<<place_grid<MAXN, 2>(P.S), 64, place_smem<2>(), st>>>(P);
   } else if (P.m >= IGP_MINB5_FROM_M && MAXN == 48) {
-    k_place<MAXN, 1, false, false, 5>
-        <<<place_grid<MAXN, 1, false, 5>(P.S), 128, place_smem<1>(), st>>>(P);
+    k_place<MAXN, 1, false, false, IGP_MINB_BIG>
+        <<<place_grid<MAXN, 1, false, IGP_MINB_BIG>(P.S), 128, place_smem<1>(), st>>>(P);
   } else {
     k_place<MAXN, 1><<<place_grid<MAXN, 1>(P.S), 128, place_smem<1>(), st>>>(P);
   }
@@ -492,6 +496,32 @@ static int launch_place_coop(PlanParams P, cudaStream_t st) {
                                  place_smem<1>(), st));
   launch_place<MAXN>(P, st);
   return IGP_E_OK;
+}
+
+// The largest dynamic shared memory one CTA of k_plan_smem may use (device limit
+// minus its static state), queried once per device.
+static size_t smem_plan_limit() {
+  static std::mutex mu;
+  static std::map<int, size_t> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t lim = optin > 4096 ? (size_t)optin - 4096 : 0;
+  cache[dev] = lim;
+  return lim;
+}
+
+// One plan per CTA with the search state in shared memory (smem_plan.cuh),
+// then the per-CTA kernel, which writes the plan (or plans a declined scenario).
+template <int MAXN>
+static void launch_smem(PlanParams P, size_t bytes, cudaStream_t st) {
+  cudaFuncSetAttribute(k_plan_smem<MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  k_plan_smem<MAXN><<<P.S, SMEM_WARPS * 32, bytes, st>>>(P);
+  launch_place<MAXN>(P, st);
 }
 
 // One scenario in windows of speculative steps (window.cuh), then the per-CTA
@@ -537,7 +567,7 @@ int igp_plan_batch_slots(int m, const double *hw, int b_max, int flags) {
                         : slots(k_place_fast<256>, 128, fast_smem(), 4);
   if (cap <= 48)
     return cta ? slots(k_place<48, 8>, 256, place_smem<8>(), 1)
-           : m >= IGP_MINB5_FROM_M ? slots(k_place<48, 1, false, false, 5>, 128, place_smem<1>(), 4)
+           : m >= IGP_MINB5_FROM_M ? slots(k_place<48, 1, false, false, IGP_MINB_BIG>, 128, place_smem<1>(), 4)
                                    : slots(k_place<48, 1>, 128, place_smem<1>(), 4);
   if (cap <= 128)
     return cta ? slots(k_place<128, 8>, 256, place_smem<8>(), 1)
@@ -609,7 +639,13 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   const bool fast = L.total > L.hand && fast_path(flags) && !P.coop;
   P.crec = fast ? (CRec *)(ws + L.crec) : nullptr;
   P.cnext = fast ? (CNext *)(ws + L.cnext) : nullptr;
-  P.hand = fast ? (Hand *)(ws + L.hand) : nullptr;
+  // IGP_F_SMEM: the shared-memory plan kernel when the scenario's state fits
+  const size_t smem_need =
+      smem_layout(m, L.pool_recs, hw.cap).total;
+  const bool smem = !fast && !P.coop && (flags & IGP_F_SMEM) && (flags & IGP_F_CTA) &&
+                    !(flags & (IGP_F_STATS | IGP_F_HWS)) && L.total > L.hand && m > 0 &&
+                    smem_need <= smem_plan_limit();
+  P.hand = (fast || smem) ? (Hand *)(ws + L.hand) : nullptr;
   // the fast kernel's decision margin; IGP_FAST_DELTA raises it (tests force the
   // exact fallback with it); it is never lowered below FAST_DELTA
   P.fast_delta = FAST_DELTA;
@@ -671,6 +707,11 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
       else if (hw.cap <= 128) rc = launch_place_coop<128>(P, st);
       else rc = launch_place_coop<256>(P, st);
       if (rc) return rc;
+    } else if (P.hand && !P.crec) {  // IGP_F_SMEM
+      const size_t bytes = smem_layout(m, P.pool_recs, hw.cap).total;
+      if (hw.cap <= 48) launch_smem<48>(P, bytes, st);
+      else if (hw.cap <= 128) launch_smem<128>(P, bytes, st);
+      else launch_smem<256>(P, bytes, st);
     } else if (hw.cap <= 48) {
       launch_place<48>(P, st);
     } else if (hw.cap <= 128) {

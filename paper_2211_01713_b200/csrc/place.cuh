@@ -44,7 +44,7 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
 #endif
 #ifndef IGP_PF_NEXT
-#define IGP_PF_NEXT 1  // L2 prefetch of the staged residents' next-unit terms
+#define IGP_PF_NEXT 0  // L2 prefetch of the staged residents' next-unit terms
 #endif
 
 #if IGP_SPLIT_NEXT
@@ -267,7 +267,7 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const bool fast = fast_path(flags);
   L.crec = off; off = align_up(off + (fast ? Sp * sizeof(CRec) : 0));
   L.cnext = off; off = align_up(off + (fast ? Sp * sizeof(CNext) : 0));
-  L.hand = off; off = align_up(off + (fast ? (size_t)S * sizeof(Hand) : 0));
+  L.hand = off; off = align_up(off + ((fast || (flags & IGP_F_SMEM)) ? (size_t)S * sizeof(Hand) : 0));
   L.total = off;
   return L;
 }

@@ -47,6 +47,7 @@ from .model import (
 DEFAULT_BATCH_CAP = 32
 IGP_F_STATS = 1
 IGP_F_CTA = 4
+IGP_F_SMEM = 8
 IGP_F_COOP = 16
 CTA_MIN_WORKLOADS = 512      # one CTA per plan: 12.6 ms vs 22.5 ms (one warp) at 1k workloads
 COOP_MIN_WORKLOADS = 10_000  # whole-GPU steps: 16.2 vs 19.5 us/step (one CTA) at 15k, 16.8 vs 23.5 at 20k;
@@ -339,6 +340,11 @@ def plan(
     flags = IGP_F_STATS if stats is not None else 0
     if m >= CTA_MIN_WORKLOADS:
         flags |= IGP_F_CTA  # one CTA per plan: many warps share each step's candidates
+    if stats is None and m < COOP_MIN_WORKLOADS:
+        # the search state in shared memory, one warp per candidate (csrc/smem_plan.cuh;
+        # the library uses the per-CTA kernel when it does not fit): C2 (1k) 7.4 vs
+        # 9.8 ms, 300 workloads 1.6 vs 2.5 ms (one CTA) / 3.0 ms (one warp)
+        flags |= IGP_F_SMEM | IGP_F_CTA
     if m >= COOP_MIN_WORKLOADS:
         # every warp of the GPU shares each step; the device falls back to the
         # per-CTA kernel when the exact sequence is needed (stats, raising input)
@@ -405,6 +411,8 @@ def _plan_block(scenarios, hw, b_max, stats, device):
     flags = IGP_F_STATS if stats is not None else 0
     if _cta_per_scenario(len(scenarios), m, device):
         flags |= IGP_F_CTA
+        if stats is None:
+            flags |= IGP_F_SMEM  # shared-memory state per CTA when it fits
     res = _device.plan_device(wl, hw_vector(hw), b_max, rank, flags=flags, device=device)
     out = []
     for s, sc in enumerate(scenarios):

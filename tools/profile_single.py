@@ -14,4 +14,4 @@ wl, names = synth.scenarios(1, m, hw, seed=2211, **kw)
 for _ in range(2):
     r = _device.plan_device(wl, hw_vector(hw), bm, name_ranks(list(names)), flags=fl, want_pred=False)
 torch.cuda.synchronize()
-print("gpus", r["gpu_count"])
+print("gpus", r["gpu_count"], "stats", r["stats"][0].tolist())

@@ -1,5 +1,6 @@
-"""Single-plan latency per kernel: one CTA (IGP_F_CTA), the windowed
-speculative kernel (IGP_F_WIN) and the grid-cooperative kernel (IGP_F_COOP).
+"""Single-plan latency per kernel: one warp, one CTA (IGP_F_CTA), the
+shared-memory CTA kernel (IGP_F_SMEM), the windowed speculative kernel
+(IGP_F_WIN) and the grid-cooperative kernel (IGP_F_COOP).
 
 usage: python tools/single_plan.py [cfg ...]   cfg = m[:r_unit[:b_max]] (default: C2 1000, 5000,
        10000, C3 100000:0.01:128).  Device-timed with CUDA events, inputs resident."""
@@ -17,6 +18,7 @@ from paper_2211_01713_b200.planner import IGP_F_COOP, IGP_F_CTA, name_ranks  # n
 from instances import make_v100  # noqa: E402
 
 IGP_F_WIN = 1 << 28
+IGP_F_SMEM = 8
 cfgs = sys.argv[1:] or ["1000", "5000", "10000", "100000:0.01:128"]
 for c in cfgs:
     parts = c.split(":")
@@ -31,9 +33,9 @@ for c in cfgs:
     hv = np.array(hw_vector(hw))
     out = {}
     units = {}
-    for tag, fl in (("cta", IGP_F_CTA), ("win", IGP_F_WIN | IGP_F_CTA),
-                    ("coop", IGP_F_COOP | IGP_F_CTA)):
-        if tag == "coop" and m < 5000:
+    for tag, fl in (("warp", 0), ("cta", IGP_F_CTA), ("smem", IGP_F_SMEM | IGP_F_CTA),
+                    ("win", IGP_F_WIN | IGP_F_CTA), ("coop", IGP_F_COOP | IGP_F_CTA)):
+        if (tag == "coop" and m < 5000) or (tag == "warp" and m > 2000) or (tag == "win" and m > 20000):
             continue
         dp = DevicePlan(wl, hv, b_max, rk, fl)
         reps = 1 if m >= 50_000 else 5

@@ -25,5 +25,7 @@ for rep in range(2):
                                    P(ws), ws.numel(), fl, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 t = st.cpu().numpy()[6:10] / m
+extra = st.cpu().numpy()[10:12]
 print(f"m={m} flags={fl}: cycles/step start+newcomer {t[0]:.0f} | candidates {t[1]:.0f} | "
-      f"post-candidates {t[2]:.0f} | commit {t[3]:.0f} | total {t.sum():.0f} ({t.sum()/1.965e3:.2f} us @1.965GHz)")
+      f"post-candidates {t[2]:.0f} | commit {t[3]:.0f} | total {t.sum():.0f} ({t.sum()/1.965e3:.2f} us @1.965GHz)"
+      f" | counters {extra.tolist()}")
