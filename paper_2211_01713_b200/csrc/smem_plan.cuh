@@ -36,24 +36,44 @@ namespace igp {
 constexpr int SMEM_WARPS = IGP_SMEM_WARPS;
 
 struct SmemLayout {
-  size_t cr, cn, hd, gst, sdesc, sj, spos, su, spool, sE, total;
+  size_t cr, cd, cd2, ska, ska1, ska2, spw, sac, sx, su, slb, hd, gst, gcap, sdesc, sj, spos, spool,
+      rows, sE, total;
 };
 
 __host__ __device__ inline size_t sm_align(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// Per placement index k (every workload is one GPU's resident once placed):
+//   cr    CRec {A = t_sch(n+1) + k_act, B = k_act * alpha_cache, cache, beta}
+//   cd / cd2  deltas {cache, power} from u to u+1 / u+1 to u+2
+//   ska / ska1 / ska2  k_act at u / u+1 / u+2
+//   spw   power at u      sac  alpha_cache     sx  {k_sch, n_kernels}
+//   su    committed units slb  lower bound
+// Per open GPU: hd (power / cache sums), gst (descriptor), gcap (tile
+// capacity), the slack order sdesc / sj / spos / sE; spool maps pool records
+// to placement indices; rows holds each warp's best unit vector.
 __host__ __device__ inline SmemLayout smem_layout(int m, long long pool_recs, int cap) {
   SmemLayout L;
   const size_t mm = (size_t)(m > 0 ? m : 1);
   size_t o = 0;
   L.cr = o; o = sm_align(o + mm * sizeof(CRec));
-  L.cn = o; o = sm_align(o + mm * sizeof(CNext));
+  L.cd = o; o = sm_align(o + mm * 16);
+  L.cd2 = o; o = sm_align(o + mm * 16);
+  L.ska = o; o = sm_align(o + mm * 8);
+  L.ska1 = o; o = sm_align(o + mm * 8);
+  L.ska2 = o; o = sm_align(o + mm * 8);
+  L.spw = o; o = sm_align(o + mm * 8);
+  L.sac = o; o = sm_align(o + mm * 8);
+  L.sx = o; o = sm_align(o + mm * 16);
+  L.su = o; o = sm_align(o + mm * 2);
+  L.slb = o; o = sm_align(o + mm * 2);
   L.hd = o; o = sm_align(o + mm * sizeof(CHead));
   L.gst = o; o = sm_align(o + mm * 8);
+  L.gcap = o; o = sm_align(o + mm * 4);
   L.sdesc = o; o = sm_align(o + mm * 8);
   L.sj = o; o = sm_align(o + mm * 4);
   L.spos = o; o = sm_align(o + mm * 4);
-  L.su = o; o = sm_align(o + mm * 2);
   L.spool = o; o = sm_align(o + (size_t)pool_recs * 2);
+  L.rows = o; o = sm_align(o + (size_t)SMEM_WARPS * (cap + 1) * 2);
   L.sE = o; o = sm_align(o + (size_t)(cap + 2) * 4);
   L.total = o;
   return L;
@@ -70,6 +90,7 @@ struct SmemCtl {
   unsigned best[2];  // step k's argmin key in best[k & 1]
   unsigned wbest[SMEM_WARPS];  // each warp's best key (its row holds the unit vector)
   int pool_top, abort_code;
+  int next_cand[2];  // step k's candidate counter in next_cand[k & 1]
 };
 
 // Step k's newcomer into buffer b: 42 LDGSTS of 16 bytes (threads 0..41).
@@ -91,42 +112,200 @@ __device__ __forceinline__ double approx_inv(double fmax, double f) {
   return fmax * r;
 }
 
-// The compact terms of the residents of GPU j (after commit_step), keyed by
-// placement index, from the full records in global memory.
-__device__ __forceinline__ void smem_compact(const ScenState &Z, CRec *cr, CNext *cn, CHead *hd,
-                                             uint16_t *su, const uint16_t *spool,
-                                             const unsigned long long *gst, int j, int lane) {
-  const unsigned long long g = gst[j];
-  const int n = (int)((g >> 16) & 0xffffu), off = (int)(g >> 32);
-  if (lane == 0) {
-    const double *gf = Z.gfold + (size_t)j * 4;
-    CHead h;
-    h.P = __ldcg(gf) + __ldcg(gf + 1);
-    h.C = __ldcg(gf + 2) + __ldcg(gf + 3);
-    hd[j] = h;
+struct SmemState {  // the shared-memory arrays of one scenario (SmemLayout)
+  CRec *cr;
+  double2 *cd, *cd2, *sx;
+  double *ska, *ska1, *ska2, *spw, *sac;
+  uint16_t *su, *slb, *spool, *rows;
+  CHead *hd;
+  unsigned long long *gst, *sdesc;
+  int32_t *gcap, *sj, *spos, *sE;
+};
+
+// The commit of step k (planner.py:312-319) by one warp, on the shared-memory
+// state: open GPU G at [need] (bk == NO_KEY) or append the newcomer to GPU j
+// with the winner's unit vector lu.  Residents whose units changed take their
+// solo terms at u and u+1 from the solo table (one L2 round trip, all lanes
+// at once); every other input is in shared memory.  The full records in
+// global memory -- read by the exact fallback and by k_place's _build_plan --
+// are written on the way (records, next-unit terms, meta, prefix fold states,
+// the GPU's fold state), with exact fp64 values and Neumaier folds in
+// resident order like commit_step.
+__device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, const ScenState &Z,
+                                            const SmemState &X, const SmemNew &NB, int k, int need,
+                                            unsigned bk, const uint16_t *lu, int G, int *poolp,
+                                            int *abortp, int lane) {
+  constexpr unsigned NO_KEY = 0xffffffffu;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int cap = hw.cap;
+  const double n_ka = NB.nw[R_KA], n_ca = NB.nw[R_CA], n_pw = NB.nw[R_PW];
+  const double ksch = NB.cold[C_KSCH], nkern = NB.cold[C_NK];
+  int j, n_old, occ_old, off;
+  if (bk == NO_KEY) {
+    j = G;
+    n_old = 0;
+    occ_old = 0;
+    off = 0;
+    if (lane == 0) {
+      off = *poolp + 1;  // records after the header slot
+      if (off + TILE0 > P.pool_recs) *abortp = IGP_E_CAPACITY;
+      else *poolp = off + TILE0;
+      X.gcap[j] = TILE0;
+    }
+    off = __shfl_sync(FULL, off, 0);
+  } else {
+    j = (int)(bk & 0x7fffffu);
+    const unsigned long long g = X.gst[j];
+    n_old = (int)((g >> 16) & 0xffffu);
+    occ_old = (int)(g & 0xffffu);
+    off = (int)(g >> 32);
+    const int tcap = X.gcap[j];
+    if (n_old + 1 > tcap) {  // grow the tile: copy it to a fresh one of twice the size
+      int noff = 0;
+      if (lane == 0) {
+        noff = *poolp + 1;
+        if (noff + 2 * tcap > P.pool_recs) *abortp = IGP_E_CAPACITY;
+        else *poolp = noff + 2 * tcap;
+      }
+      noff = __shfl_sync(FULL, noff, 0);
+      __syncwarp();
+      if (*(volatile int *)abortp == 0) {
+        for (int r = lane; r < n_old; r += 32) {
+#pragma unroll
+          for (int f = 0; f < R_NF; ++f)
+            Z.rec[(size_t)(noff + r) * R_NF + f] = Z.rec[(size_t)(off + r) * R_NF + f];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) Z.nxt[(size_t)(noff + r) * 4 + f] = Z.nxt[(size_t)(off + r) * 4 + f];
+          Z.meta[noff + r] = Z.meta[off + r];
+          X.spool[noff + r] = X.spool[off + r];
+        }
+        if (lane == 0) X.gcap[j] = 2 * tcap;
+        off = noff;
+      }
+      __syncwarp();
+    }
   }
+  if (*(volatile int *)abortp) return;
+  const int n = n_old + 1;
+  const double dnext = delta_sch(hw, n + 1);  // t_sch for the next candidate size
+  int part = 0;
+  double f_pw = 0.0, f_ca = 0.0;  // fold inputs of resident `lane`
   for (int r = lane; r < n; r += 32) {
-    const int kk = spool[off + r];
-    const double *rr = Z.rec + (size_t)(off + r) * R_NF;
-    const double ka = __ldcg(rr + R_KA), ca = __ldcg(rr + R_CA), tsn = __ldcg(rr + R_TSN);
-    const double ac = __ldcg(rr + R_ACACHE), pw = __ldcg(rr + R_PW);
+    const bool nwc = r == n_old;
+    const int kk = nwc ? k : (int)X.spool[off + r];
+    const int nu = lu ? (int)lu[r] : need;
+    double *rr = Z.rec + (size_t)(off + r) * R_NF;
+    if (nwc) {  // the newcomer's constants (planner.py:291-292)
+      X.spool[off + r] = (uint16_t)k;
+      X.sx[kk] = make_double2(ksch, nkern);
+      X.sac[kk] = NB.nw[R_ACACHE];
+      X.slb[kk] = (uint16_t)need;
+      rr[R_ACACHE] = NB.nw[R_ACACHE];
+      rr[R_TLOAD] = NB.nw[R_TLOAD];
+      rr[R_TFB] = NB.nw[R_TFB];
+      rr[R_THALF] = NB.nw[R_THALF];
+    }
+    const bool changed = nwc || nu != (int)X.su[kk];
+    double ca_x;
+    if (changed) {  // solo terms at nu, nu + 1, nu + 2 (model.py:285-297)
+      Solo so, s1, s2;
+      if (nwc) {
+        const int v = nu - need;
+        auto at = [&](int vv, int uu) {
+          if (vv == 0) return Solo{n_ka, n_pw, n_ca, 0};
+          if (vv < TB && uu <= cap)
+            return Solo{NB.ntab[vv * 4], NB.ntab[vv * 4 + 1], NB.ntab[vv * 4 + 2],
+                        (int)NB.ntab[vv * 4 + 3]};
+          return solo_from_cold(NB.cold, (double)uu * hw.runit);
+        };
+        so = at(v, nu);
+        s1 = at(v + 1, nu + 1);
+        s2 = at(v + 2, nu + 2);
+      } else {
+        const int lb = X.slb[kk];
+        so = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu);
+        s1 = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu + 1);
+        s2 = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu + 2);
+      }
+      X.ska2[kk] = s2.ka;
+      X.cd2[kk] = make_double2(s2.ca - s1.ca, s2.pw - s1.pw);
+      X.ska[kk] = so.ka;
+      X.spw[kk] = so.pw;
+      X.ska1[kk] = s1.ka;
+      X.cd[kk] = make_double2(s1.ca - so.ca, s1.pw - so.pw);
+      X.su[kk] = (uint16_t)nu;
+      rr[R_KA] = so.ka;
+      rr[R_CA] = so.ca;
+      rr[R_PW] = so.pw;
+      double *nx = Z.nxt + (size_t)(off + r) * 4;
+      nx[0] = s1.ka;
+      nx[1] = s1.pw;
+      nx[2] = s1.ca;
+      nx[3] = (double)s1.err;
+      Z.meta[off + r] = Meta{kk, (uint16_t)nu, X.slb[kk]};
+      ca_x = so.ca;
+    } else {
+      ca_x = X.cr[kk].ca;
+    }
+    const double2 xs = X.sx[kk];
+    const double tsn = (xs.x + dnext) * xs.y;
+    rr[R_TSN] = tsn;
+    const double ka = X.ska[kk];
     CRec c;
     c.A = tsn + ka;
-    c.B = ka * ac;
-    c.ca = ca;
-    c.beta = fast_beta(__ldcg(rr + R_THALF), __ldcg(rr + R_TLOAD), __ldcg(rr + R_TFB));
-    cr[kk] = c;
-    const double *nx = Z.nxt + (size_t)(off + r) * 4;
-    const double ka1 = __ldcg(nx), pw1 = __ldcg(nx + 1), ca1 = __ldcg(nx + 2);
-    CNext q;
-    q.A1 = tsn + ka1;
-    q.B1 = ka1 * ac;
-    q.dca = ca1 - ca;
-    q.dpw = pw1 - pw;
-    cn[kk] = q;
-    const unsigned long long mv = __ldcg(reinterpret_cast<const unsigned long long *>(Z.meta + off + r));
-    su[kk] = reinterpret_cast<const Meta *>(&mv)->u;
+    c.B = ka * X.sac[kk];
+    c.ca = ca_x;
+    c.beta = nwc ? fast_beta(NB.nw[R_THALF], NB.nw[R_TLOAD], NB.nw[R_TFB]) : X.cr[kk].beta;
+    X.cr[kk] = c;
+    if (r < 32) {
+      f_pw = X.spw[kk];
+      f_ca = ca_x;
+    }
+    part += nu;
   }
+  part = warp_sum(part);
+  __syncwarp();
+  // exact prefix fold states of this GPU, in resident order (model.py:299/304)
+  Neumaier fp, fc;
+  fp.s = fp.c = fc.s = fc.c = 0.0;  // as commit_step (an add from zero is Neumaier.first)
+  for (int r = 0; r < n; ++r) {
+    double pw, ca;
+    if (r < 32) {
+      pw = __shfl_sync(FULL, f_pw, r);
+      ca = __shfl_sync(FULL, f_ca, r);
+    } else {
+      const int kk = X.spool[off + r];
+      pw = X.spw[kk];
+      ca = X.cr[kk].ca;
+    }
+    if (lane == 0) {
+      double *pp = Z.pfx + (size_t)(off + r) * 4;
+      pp[0] = fp.s;
+      pp[1] = fp.c;
+      pp[2] = fc.s;
+      pp[3] = fc.c;
+    }
+    fp.add(pw);
+    fc.add(ca);
+  }
+  const unsigned long long desc = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
+  if (lane == 0) {
+    double *gf = Z.gfold + (size_t)j * 4;
+    gf[0] = fp.s;
+    gf[1] = fp.c;
+    gf[2] = fc.s;
+    gf[3] = fc.c;
+    CHead h;
+    h.P = fp.s + fp.c;
+    h.C = fc.s + fc.c;
+    X.hd[j] = h;
+    X.gst[j] = desc;
+  }
+  __syncwarp();
+  if (bk == NO_KEY)
+    slack_insert(X.sj, X.spos, X.sdesc, X.sE, j, desc, cap - need, lane);
+  else
+    slack_move_down(X.sj, X.spos, X.sdesc, X.sE, j, desc, cap - occ_old, cap - part, lane);
 }
 
 template <int MAXN>
@@ -145,27 +324,43 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
     return;
   }
   const SmemLayout SL = smem_layout(m, P.pool_recs, P.cap_ld);
-  CRec *const cr = reinterpret_cast<CRec *>(dsm + SL.cr);
-  CNext *const cn = reinterpret_cast<CNext *>(dsm + SL.cn);
-  CHead *const hd = reinterpret_cast<CHead *>(dsm + SL.hd);
-  unsigned long long *const gst = reinterpret_cast<unsigned long long *>(dsm + SL.gst);
-  unsigned long long *const sdesc = reinterpret_cast<unsigned long long *>(dsm + SL.sdesc);
-  int32_t *const sj = reinterpret_cast<int32_t *>(dsm + SL.sj);
-  int32_t *const spos = reinterpret_cast<int32_t *>(dsm + SL.spos);
-  uint16_t *const su = reinterpret_cast<uint16_t *>(dsm + SL.su);
-  uint16_t *const spool = reinterpret_cast<uint16_t *>(dsm + SL.spool);
-  int32_t *const sE = reinterpret_cast<int32_t *>(dsm + SL.sE);
+  SmemState X;
+  X.cr = reinterpret_cast<CRec *>(dsm + SL.cr);
+  X.cd = reinterpret_cast<double2 *>(dsm + SL.cd);
+  X.cd2 = reinterpret_cast<double2 *>(dsm + SL.cd2);
+  X.ska = reinterpret_cast<double *>(dsm + SL.ska);
+  X.ska1 = reinterpret_cast<double *>(dsm + SL.ska1);
+  X.ska2 = reinterpret_cast<double *>(dsm + SL.ska2);
+  X.spw = reinterpret_cast<double *>(dsm + SL.spw);
+  X.sac = reinterpret_cast<double *>(dsm + SL.sac);
+  X.sx = reinterpret_cast<double2 *>(dsm + SL.sx);
+  X.su = reinterpret_cast<uint16_t *>(dsm + SL.su);
+  X.slb = reinterpret_cast<uint16_t *>(dsm + SL.slb);
+  X.hd = reinterpret_cast<CHead *>(dsm + SL.hd);
+  X.gst = reinterpret_cast<unsigned long long *>(dsm + SL.gst);
+  X.gcap = reinterpret_cast<int32_t *>(dsm + SL.gcap);
+  X.sdesc = reinterpret_cast<unsigned long long *>(dsm + SL.sdesc);
+  X.sj = reinterpret_cast<int32_t *>(dsm + SL.sj);
+  X.spos = reinterpret_cast<int32_t *>(dsm + SL.spos);
+  X.spool = reinterpret_cast<uint16_t *>(dsm + SL.spool);
+  X.rows = reinterpret_cast<uint16_t *>(dsm + SL.rows);
+  X.sE = reinterpret_cast<int32_t *>(dsm + SL.sE);
+  CRec *const cr = X.cr;
+  CHead *const hd = X.hd;
+  unsigned long long *const gst = X.gst;
+  unsigned long long *const sdesc = X.sdesc;
+  int32_t *const sj = X.sj, *const sE = X.sE;
+  uint16_t *const su = X.su, *const spool = X.spool;
 
   const size_t sm = (size_t)s * m;
   const double *cold = P.cold + sm * C_NF;
   const double *nwt = P.nw + sm * R_NF;
   const double *tbl = P.tbl + sm * TB * 4;
   const size_t sp = (size_t)s * (size_t)P.pool_recs;
-  const ScenState Z{cold, tbl, gst, sdesc, sj, spos, sE, P.gcap + sm, P.gfold + sm * 4,
+  const ScenState Z{cold, tbl, gst, sdesc, sj, X.spos, sE, P.gcap + sm, P.gfold + sm * 4,
                     P.rec + sp * R_NF, P.nxt + sp * 4, P.frec + sp * 2, P.pfx + sp * 4,
                     P.meta + sp, sm};
-  uint16_t *const rows = P.lane_units + (size_t)s * P.lanes * P.cap_ld;
-  uint16_t *const my_row = rows + (size_t)wi * cap;
+  uint16_t *const my_row = X.rows + (size_t)wi * (cap + 1);
   for (int x = t; x < cap + 2; x += blockDim.x) sE[x] = 0;
   if (t == 0) {
     ctl.pool_top = 0;
@@ -175,7 +370,10 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
   unsigned long long evals = 0, cands = 0, exact = 0;
   const double delta = P.fast_delta;
   smem_fetch_newcomer(ctl.nb[P.k0 & 1], nwt, cold, tbl, P.k0, t);
-  if (t == 0) ctl.best[0] = ctl.best[1] = NO_KEY;
+  if (t == 0) {
+    ctl.best[0] = ctl.best[1] = NO_KEY;
+    ctl.next_cand[0] = ctl.next_cand[1] = 0;
+  }
   cp_async_wait_all();
   __syncthreads();
   for (int k = P.k0; k < P.k1; ++k) {
@@ -198,7 +396,14 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
     unsigned w_best = NO_KEY;  // this warp's best key (its row holds the unit vector)
 
     // ---- candidates: one warp each (planner.py:296-311) ----
-    for (int c = wi; c < ncand; c += SMEM_WARPS) {
+    // warps take the step's candidates from a shared counter: a long Alg. 2
+    // chain does not hold back a candidate statically assigned behind it
+    int* const ncp = &ctl.next_cand[k & 1];
+    for (;;) {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(ncp, 1);
+      c = __shfl_sync(FULL, c, 0);
+      if (c >= ncand) break;
       const int j = sj[c];
       const unsigned long long g = sdesc[c];
       if ((((unsigned)need << 23) | (unsigned)j) > *(volatile unsigned *)bestp) continue;
@@ -295,22 +500,28 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
                 cur_ca = so.ca;
                 cur_pw = so.pw;
               } else if (bumps == 0) {  // one unit above the committed units
-                const CNext q = cn[kk];
-                A = q.A1;
-                B = q.B1;
-                ca += q.dca;
-                dC = q.dca;
-                dP = q.dpw;
+                const double2 q = X.cd[kk];
+                A += X.ska1[kk] - X.ska[kk];
+                B = X.ska1[kk] * X.sac[kk];
+                ca += q.x;
+                dC = q.x;
+                dP = q.y;
+              } else if (bumps == 1) {  // two units above: also precomputed
+                const double2 q = X.cd2[kk];
+                A += X.ska2[kk] - X.ska1[kk];
+                B = X.ska2[kk] * X.sac[kk];
+                ca += q.x;
+                dC = q.x;
+                dP = q.y;
               } else {  // further bumps: the solo table at the new units
 #if IGP_TIMING
                 if (s == 0 && P.stats) atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 4], 1ull);
 #endif
-                const Meta mt = Z.meta[off + i];
-                const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u);
-                const Solo s0 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, u - 1);
-                const double *rr = Z.rec + (size_t)(off + i) * R_NF;
-                A = rr[R_TSN] + so.ka;
-                B = so.ka * rr[R_ACACHE];
+                const int lb = X.slb[kk];
+                const Solo so = solo_lookup(tbl, cold, hw, kk, lb, u);
+                const Solo s0 = solo_lookup(tbl, cold, hw, kk, lb, u - 1);
+                A += so.ka - s0.ka;
+                B = so.ka * X.sac[kk];
                 ca = so.ca;
                 dC = so.ca - s0.ca;
                 dP = so.pw - s0.pw;
@@ -365,28 +576,16 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
 #endif
     // ---- commit (planner.py:312-319), warp 0 ----
     if (wi == 0) {
-      const int jj = bk == NO_KEY ? G : (int)(bk & 0x7fffffu);
-      const int nres = bk == NO_KEY ? 0 : (int)((gst[jj] >> 16) & 0xffffu);
-      const int off0 = bk == NO_KEY ? 0 : (int)(gst[jj] >> 32);
       const unsigned wb = lane < SMEM_WARPS ? ctl.wbest[lane] : NO_KEY;
       const unsigned hit = __ballot_sync(FULL, bk != NO_KEY && wb == bk);
-      const uint16_t *lu_w = bk != NO_KEY ? rows + (size_t)(__ffs(hit) - 1) * cap : nullptr;
-      commit_step(P, hw, Z, k, need, bk, lu_w, G, &ctl.pool_top, &ctl.abort_code, NB.nw, ksch,
-                  nkern, lane);
-      __syncwarp();
-      if (!*(volatile int *)&ctl.abort_code) {
-        // the resident lists follow the tile (moved when it grew)
-        const int off1 = (int)(gst[jj] >> 32);
-        if (off1 != off0)
-          for (int r = lane; r < nres; r += 32) spool[off1 + r] = spool[off0 + r];
-        if (lane == 0) spool[off1 + nres] = (uint16_t)k;
-        __syncwarp();
-        __threadfence_block();
-        smem_compact(Z, cr, cn, hd, su, spool, gst, jj, lane);
-      }
+      const uint16_t *lu_w = bk != NO_KEY ? X.rows + (size_t)(__ffs(hit) - 1) * (cap + 1) : nullptr;
+      commit_smem(P, hw, Z, X, NB, k, need, bk, lu_w, G, &ctl.pool_top, &ctl.abort_code, lane);
     }
     if (bk == NO_KEY) G += 1;
-    if (t == 0) ctl.best[(k + 1) & 1] = NO_KEY;  // nobody reads it during step k
+    if (t == 0) {  // step k+1's slots: nobody reads them during step k
+      ctl.best[(k + 1) & 1] = NO_KEY;
+      ctl.next_cand[(k + 1) & 1] = 0;
+    }
     cp_async_wait_all();  // step k+1's newcomer
     __syncthreads();
 #if IGP_TIMING

@@ -342,8 +342,8 @@ def plan(
         flags |= IGP_F_CTA  # one CTA per plan: many warps share each step's candidates
     if stats is None and m < COOP_MIN_WORKLOADS:
         # the search state in shared memory, one warp per candidate (csrc/smem_plan.cuh;
-        # the library uses the per-CTA kernel when it does not fit): C2 (1k) 7.4 vs
-        # 9.8 ms, 300 workloads 1.6 vs 2.5 ms (one CTA) / 3.0 ms (one warp)
+        # the library uses the per-CTA kernel when it does not fit): C2 (1k) 5.4 vs
+        # 9.8 ms, 300 workloads 1.25 vs 2.5 ms (one CTA) / 3.0 ms (one warp)
         flags |= IGP_F_SMEM | IGP_F_CTA
     if m >= COOP_MIN_WORKLOADS:
         # every warp of the GPU shares each step; the device falls back to the
