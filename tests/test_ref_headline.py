@@ -112,13 +112,14 @@ def test_plan_api_matches_reference_10k(cuda, with_stats):
 
 @pytest.mark.gpu
 def test_batch_abi_matches_reference_10k_inside_full_batch(cuda):
-    """The headline path: scenario 0 (and a copy of it at the LAST index of a
-    2,368-scenario batch, so an offset bug at the far end shows) planned by
-    igp_plan_batch_host / igp_plan_batch_device at the bench's batch size."""
+    """The headline path: scenario 0 (and copies of it in the middle and at the
+    LAST index of the bench's batch -- two waves of the place kernel's resident
+    slots, 5,920 scenarios on a B200 -- so an offset bug at the far end shows)
+    planned by igp_plan_batch_host / igp_plan_batch_device."""
     from paper_2211_01713_b200 import _device
     from paper_2211_01713_b200.planner import name_ranks
     d = G.load("ref_plan_10k")
-    S = 2368
+    S = 2 * _device.batch_slots(10_000, _hv(), 32)  # bench.py: WAVES x slots
     wl = np.empty((S, 16, 10_000))
     wl[:] = d["wl"][None]
     rank = name_ranks(list(d["names"]))

@@ -36,7 +36,7 @@ import torch  # noqa: E402
 
 from paper_2211_01713_b200 import _device, _native, synth  # noqa: E402
 from paper_2211_01713_b200.layout import hw_vector  # noqa: E402
-from paper_2211_01713_b200.planner import IGP_F_COOP, IGP_F_CTA, IGP_F_STATS, name_ranks  # noqa: E402
+from paper_2211_01713_b200.planner import IGP_F_COOP, IGP_F_CTA, IGP_F_SMEM, IGP_F_STATS, name_ranks  # noqa: E402
 
 dev = torch.device("cuda", 0)
 lib = _native.lib_for_compute()
@@ -112,7 +112,7 @@ def c1():
     api_ms = (time.perf_counter() - t0) / n * 1e3
     wl = np.stack([np.array(igp.planner.workload_table(w))])
     rk = name_ranks([s.name for s, _ in w])
-    dp = DevicePlan(wl, np.array(hw_vector(hw)), 32, rk, 0)
+    dp = DevicePlan(wl, np.array(hw_vector(hw)), 32, rk, IGP_F_SMEM | IGP_F_CTA)  # plan()'s kernel
     dev_ms = dp.time(20)
     t0 = time.perf_counter()
     for _ in range(200):
@@ -131,7 +131,8 @@ def c2():
     wl, names = synth.scenarios(1, 1000, hw, seed=7)
     rk = name_ranks(list(names))
     out = {}
-    for tag, fl in (("warp", 0), ("cta", IGP_F_CTA), ("coop", IGP_F_COOP | IGP_F_CTA)):
+    for tag, fl in (("warp", 0), ("cta", IGP_F_CTA), ("coop", IGP_F_COOP | IGP_F_CTA),
+                    ("smem", IGP_F_SMEM | IGP_F_CTA)):
         dp = DevicePlan(wl, hv, 32, rk, fl)
         out[tag] = dp.time(10)
     st = dp.ref_stats()
@@ -143,7 +144,8 @@ def c2():
     emit(dict(config="C2", workload="1 plan of 1,000 synthetic workloads, r_unit 0.025, b<=32",
               cpu_oracle_ms_per_plan_1core=cpu_ms,
               ms_per_plan_warp=out["warp"], ms_per_plan_cta=out["cta"],
-              ms_per_plan_coop=out["coop"],
+              ms_per_plan_coop=out["coop"], ms_per_plan_smem=out["smem"],
+              kernel_plan_api="smem (IGP_F_SMEM | IGP_F_CTA: shared-memory state, warp per candidate)",
               us_per_step=min(out.values()) * 1e3 / 1000, reference_counters=st,
               candidate_evals_per_s=st["model_evals"] / (min(out.values()) / 1e3)))
 
