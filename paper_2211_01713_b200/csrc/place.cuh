@@ -43,6 +43,12 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #ifndef IGP_NW_SMEM
 #define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
 #endif
+#ifndef IGP_PF_DESC
+#define IGP_PF_DESC 0  // L1 prefetch of the next refill's slack-order descriptors
+#endif
+#ifndef IGP_PF_NEXT_L1
+#define IGP_PF_NEXT_L1 0  // L1 prefetch of the first staged residents' next-unit terms
+#endif
 #ifndef IGP_PF_NEXT
 #define IGP_PF_NEXT 0  // L2 prefetch of the staged residents' next-unit terms
 #endif
@@ -1311,6 +1317,9 @@ k_place(PlanParams P) {
                   bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, lbar);
 #endif
                   c_wait = true;
+#if IGP_SPLIT_NEXT && IGP_PF_NEXT_L1
+                  asm volatile("prefetch.global.L1 [%0];" ::"l"(NEXT_AT(c_off)));
+#endif
 #if IGP_SPLIT_NEXT && IGP_PF_NEXT
                   // the staged residents' next-unit terms, read on their first
                   // bump: L2 prefetch of their lines.  +1.5% at the headline
@@ -1356,6 +1365,17 @@ k_place(PlanParams P) {
             }
           }
           qhead += nidle;
+#if IGP_PF_DESC
+          // the next refill's slack-order descriptors: into L1 now, so the
+          // next refill's sj / sdesc loads do not wait on L2 or DRAM
+          if constexpr (GW == 1 && !COOP && !serial) {
+            const int pp = qhead + lane;
+            if (pp < ncand && (lane & 7) == 0) {
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(sdesc + pp));
+              if ((lane & 15) == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(sj + pp));
+            }
+          }
+#endif
 #if IGP_PF_BATCH
           // the next refill's candidates: load their descriptors now (used
           // only after this iteration's tile waits, so the load is not on the
