@@ -44,10 +44,7 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
 #endif
 #ifndef IGP_PF_DESC
-#define IGP_PF_DESC 0  // L1 prefetch of the next refill's slack-order descriptors
-#endif
-#ifndef IGP_PF_NEXT_L1
-#define IGP_PF_NEXT_L1 0  // L1 prefetch of the first staged residents' next-unit terms
+#define IGP_PF_DESC 1  // L1 prefetch of the next refill's slack-order descriptors
 #endif
 #ifndef IGP_PF_NEXT
 #define IGP_PF_NEXT 0  // L2 prefetch of the staged residents' next-unit terms
@@ -1317,9 +1314,6 @@ k_place(PlanParams P) {
                   bulk_g2s(sl->gf, rec + (size_t)(c_off - 1) * R_NF, bytes, lbar);
 #endif
                   c_wait = true;
-#if IGP_SPLIT_NEXT && IGP_PF_NEXT_L1
-                  asm volatile("prefetch.global.L1 [%0];" ::"l"(NEXT_AT(c_off)));
-#endif
 #if IGP_SPLIT_NEXT && IGP_PF_NEXT
                   // the staged residents' next-unit terms, read on their first
                   // bump: L2 prefetch of their lines.  +1.5% at the headline
