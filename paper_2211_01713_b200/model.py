@@ -257,13 +257,16 @@ def gpu_frequency(hw: HardwareProfile, p_demand: float) -> float:
 class _Entry:
     """A (spec, coefficients, batch) triple prepared for device evaluation.
 
-    Stands in for the reference's pre-reduced constants (model.py:239-270);
-    the constants themselves are formed on the device (k_build / row_entry).
-    ``t_half`` and ``rate_rps`` are kept because callers compare against them
-    (planner.py:158, oracle.py:73).
+    The device forms the pre-reduced constants itself (k_build / row_entry);
+    this host object keeps ``spec`` and ``coef`` for marshalling and exposes
+    the reference's attributes (model.py:239-270: ``gamma``, ``k4`` ...
+    ``t_load``, ``t_feedback``, ``t_half``, ``rate_rps``), so modules that
+    import ``_Entry`` (oracle.py:16-22, baselines.py:19-28) read the same
+    values.  They are formed on first access with the reference's operations
+    in the reference's order (CPython floats: identical bits).
     """
 
-    __slots__ = ("name", "batch", "spec", "coef", "t_half", "rate_rps")
+    __slots__ = ("name", "batch", "spec", "coef", "t_half", "rate_rps", "_hw")
 
     def __init__(self, spec, coef, batch: int, hw=None):
         self.name = spec.name
@@ -272,6 +275,30 @@ class _Entry:
         self.coef = coef
         self.t_half = spec.slo_ms / 2.0
         self.rate_rps = spec.rate_rps
+        self._hw = hw
+
+    @property
+    def gamma(self):
+        c, b = self.coef, self.batch
+        return c.k1 * b * b + c.k2 * b + c.k3
+
+    k4 = property(lambda self: self.coef.k4)
+    k5 = property(lambda self: self.coef.k5)
+    k_sch = property(lambda self: self.coef.k_sch_ms)
+    n_kernels = property(lambda self: self.coef.n_kernels)
+    alpha_cache = property(lambda self: self.coef.alpha_cache)
+    alpha_p = property(lambda self: self.coef.alpha_power_w)
+    beta_p = property(lambda self: self.coef.beta_power_w)
+    alpha_c = property(lambda self: self.coef.alpha_cacheutil)
+    beta_c = property(lambda self: self.coef.beta_cacheutil)
+
+    @property
+    def t_load(self):
+        return self.spec.d_load_mb * self.batch / self._hw.pcie_bw_mb_per_ms
+
+    @property
+    def t_feedback(self):
+        return self.spec.d_feedback_mb * self.batch / self._hw.pcie_bw_mb_per_ms
 
 
 def _states_to_arrays(states):

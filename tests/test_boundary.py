@@ -143,3 +143,19 @@ def test_stub_plan_matches_reference_fixtures(tmp_path, monkeypatch, case):
             assert np.float64(g.predicted[a.workload].t_inf_ms).view(np.int64) == \
                 G.bits(d["pred"][i, 6])
     assert p.cost_per_hour == float(d["cost"])
+
+
+def test_entry_exposes_the_reference_constants():
+    """_Entry keeps the reference's attributes (model.py:239-270) bit for bit."""
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    gm = pytest.importorskip("gpuplanner.model")
+    from paper_2211_01713_b200 import model as mm
+    from instances import make_v100, random_instance
+    import numpy as np
+    hw = make_v100()
+    for spec, coef in random_instance(np.random.default_rng(3), 20, hw):
+        b = 1 + len(spec.name) % 7
+        ours, ref = mm._Entry(spec, coef, b, hw), gm._Entry(spec, coef, b, hw)
+        for a in gm._Entry.__slots__:
+            assert getattr(ours, a) == getattr(ref, a), a

@@ -36,4 +36,20 @@ simulate(igp.plan(inst[:4], hw), {s.name: s for s, _ in inst}, {s.name: c for s,
 _device.components(wl[0][:, :64], np.arange(1, 65), np.full(64, 0.1), np.full(64, 0.5),
                    np.arange(64) % 9, np.linspace(100.0, 500.0, 64), hv)
 igp.power_demand(hw, [50.0, 60.5, 70.25]); igp.power_demand(hw, [])
+# round 2: the shared-memory plan kernel (one CTA per scenario; a declined
+# scenario and the wide-margin exact path), the certified-margin batch kernel,
+# select_gpu_type in one launch
+IGP_F_SMEM, IGP_F_FAST = 8, 1 << 29
+w2, n2 = synth.scenarios(3, 400, hw, seed=5)
+r2 = name_ranks(list(n2))
+_device.plan_device(w2[:1], hv, 32, r2, flags=IGP_F_SMEM | IGP_F_CTA)
+w2b = w2.copy(); w2b[1, 0, 10] = 1e-3  # a prologue error: declined
+_device.plan_device(w2b, hv, 32, r2, flags=IGP_F_SMEM | IGP_F_CTA)
+os.environ["IGP_FAST_DELTA"] = "0.5"
+_device.plan_device(w2[:1], hv, 32, r2, flags=IGP_F_SMEM | IGP_F_CTA)
+_device.plan_device(w2, hv, 32, r2, flags=IGP_F_FAST)
+del os.environ["IGP_FAST_DELTA"]
+_device.plan_device(w2, hv, 32, r2, flags=IGP_F_FAST)
+igp.select_gpu_type([s for s, _ in inst], [hw, make_v100(gpu_type="b", r_unit=0.05)],
+                    {"v100": {s.name: c for s, c in inst}, "b": {s.name: c for s, c in inst}})
 print("sanitize workload done")
