@@ -143,25 +143,34 @@ def _plan_device_once(wl, hw_vec, b_max, rank, flags, device, want_pred):
     with torch.cuda.device(device):
         d_wl = _to_dev(wl, device)
         d_rank = _to_dev(rank, device)
-        i32 = torch.empty((5, S, max(m, 1)), dtype=torch.int32, device=device)
-        d_pred = torch.empty((S, max(m, 1), 10), dtype=torch.float64, device=device) if want_pred else None
-        d_gc = torch.empty(S, dtype=torch.int32, device=device)
-        d_st = torch.empty((S, 6), dtype=torch.int64, device=device)
-        d_err = torch.empty((S, ctypes.sizeof(_native.IgpError)), dtype=torch.uint8, device=device)
+        # every output in one device buffer (one D2H copy): fp64 rows first,
+        # then stats (int64), the int32 arrays and the error records
+        mm = max(m, 1)
+        n_pred = S * mm * 10 if want_pred else 0
+        esz = ctypes.sizeof(_native.IgpError)
+        o_st = n_pred * 8
+        o_i32 = o_st + S * 6 * 8
+        o_gc = o_i32 + 5 * S * mm * 4
+        o_err = (o_gc + S * 4 + 7) // 8 * 8
+        out = torch.empty(o_err + S * esz, dtype=torch.uint8, device=device)
+        base = out.data_ptr()
+        vp = ctypes.c_void_p
+        i32p = [vp(base + o_i32 + f * S * mm * 4) for f in range(5)]
         nbytes = plan_workspace_bytes(S, m, h, b_max, flags)
         ws = workspace(nbytes, device)
         rc = lib.igp_plan_batch_device(
             _ptr(d_wl), S, m, _np_ptr(h), int(b_max), _ptr(d_rank), rank_stride,
-            _ptr(i32[0]), _ptr(i32[1]), _ptr(i32[2]), _ptr(i32[3]), _ptr(i32[4]),
-            _ptr(d_pred), _ptr(d_gc), _ptr(d_st), _ptr(d_err), _ptr(ws), ws.numel(),
-            int(flags), _stream(device))
+            *i32p, vp(base) if want_pred else vp(0), vp(base + o_gc), vp(base + o_st),
+            vp(base + o_err), _ptr(ws), ws.numel(), int(flags), _stream(device))
         _check(rc)
-        out_i = i32.cpu().numpy()[:, :, :m]
+        host = out.cpu().numpy()
+        out_i = host[o_i32:o_gc].view(np.int32).reshape(5, S, mm)[:, :, :m]
         res = dict(gpu_of=out_i[0], pos=out_i[1], units=out_i[2], batch=out_i[3], lb=out_i[4],
-                   gpu_count=d_gc.cpu().numpy(), stats=d_st.cpu().numpy(),
-                   err=d_err.cpu().numpy().view(_native.err_dtype()).reshape(S))
+                   gpu_count=host[o_gc:o_gc + S * 4].view(np.int32),
+                   stats=host[o_st:o_i32].view(np.int64).reshape(S, 6),
+                   err=host[o_err:].view(_native.err_dtype()).reshape(S))
         if want_pred:
-            res["pred"] = d_pred.cpu().numpy()[:, :m]
+            res["pred"] = host[:n_pred * 8].view(np.float64).reshape(S, mm, 10)[:, :m]
     return res
 
 

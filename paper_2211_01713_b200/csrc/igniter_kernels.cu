@@ -643,7 +643,7 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   const size_t smem_need =
       smem_layout(m, L.pool_recs, hw.cap).total;
   const bool smem = !fast && !P.coop && (flags & IGP_F_SMEM) && (flags & IGP_F_CTA) &&
-                    !(flags & (IGP_F_STATS | IGP_F_HWS)) && L.total > L.hand && m > 0 &&
+                    !(flags & IGP_F_STATS) && L.total > L.hand && m > 0 &&
                     smem_need <= smem_plan_limit();
   P.hand = (fast || smem) ? (Hand *)(ws + L.hand) : nullptr;
   // the fast kernel's decision margin; IGP_FAST_DELTA raises it (tests force the

@@ -751,6 +751,7 @@ __device__ __forceinline__ void commit_step(const PlanParams &P, const Hw &hw, c
         hd->gf[2] = fc.s;
         hd->gf[3] = fc.c;
         hd->meta[0] = meta[off];
+        hd->meta[1] = hd->meta[2] = hd->meta[3] = Meta{0, 0, 0};  // staged by tile copies
         if (P.stream) {
           P.gpu_of[sm + k] = G;
           P.pos[sm + k] = 0;
@@ -903,7 +904,7 @@ __device__ __forceinline__ void commit_step(const PlanParams &P, const Hw &hw, c
         hd->gf[1] = fp.c;
         hd->gf[2] = fc.s;
         hd->gf[3] = fc.c;
-        for (int r = 0; r < n && r < 4; ++r)
+        for (int r = 0; r < 4; ++r)  // entries past n are zero (staged by tile copies)
           *reinterpret_cast<unsigned long long *>(&hd->meta[r]) = hmeta[r];
         if (P.stream) {
           P.gpu_of[sm + k] = j;

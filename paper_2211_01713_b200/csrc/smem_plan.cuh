@@ -317,7 +317,10 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
   const int t = threadIdx.x, lane = t & 31, wi = t >> 5;
   const int s = blockIdx.x;
   Hand *const hdp = P.hand + s;
-  const Hw &hw = P.hw;
+  __shared__ Hw shw;  // the scenario's profile (IGP_F_HWS: one per scenario)
+  if (t == 0) shw = P.hw_s ? P.hw_s[s] : P.hw;
+  __syncthreads();
+  const Hw &hw = shw;
   const int m = P.m, cap = hw.cap;
   if (P.perr[s] != INT_MAX || P.sflags[s] != 0 || !hw.margin_ok) {
     if (t == 0) hdp->k_done = P.k0;  // declined: k_place plans it

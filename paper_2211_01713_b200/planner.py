@@ -465,7 +465,12 @@ def select_gpu_type(
         n = len(tables)
         rank = name_ranks([s.name for s in workloads])
         hv = np.stack([np.asarray(hw_vector(hw), np.float64) for hw in profiles[:n]])
-        flags = IGP_F_CTA if _cta_per_scenario(n, len(workloads)) else 0
+        if n <= _device.sm_count():
+            # one CTA per type with the search state in shared memory (the library
+            # falls back to the per-CTA kernel when it does not fit): 4 types x 1k
+            flags = IGP_F_SMEM | IGP_F_CTA
+        else:
+            flags = IGP_F_CTA if _cta_per_scenario(n, len(workloads)) else 0
         res = _device.plan_device(np.stack(tables), hv, b_max, rank, flags=flags)
     best: Plan | None = None
     last_error: Exception | None = None
