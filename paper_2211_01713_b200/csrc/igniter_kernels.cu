@@ -519,8 +519,14 @@ static size_t smem_plan_limit() {
 // then the per-CTA kernel, which writes the plan (or plans a declined scenario).
 template <int MAXN>
 static void launch_smem(PlanParams P, size_t bytes, cudaStream_t st) {
-  cudaFuncSetAttribute(k_plan_smem<MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  k_plan_smem<MAXN><<<P.S, SMEM_WARPS * 32, bytes, st>>>(P);
+  if (P.hw_s) {
+    cudaFuncSetAttribute(k_plan_smem<MAXN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bytes);
+    k_plan_smem<MAXN, true><<<P.S, SMEM_WARPS * 32, bytes, st>>>(P);
+  } else {
+    cudaFuncSetAttribute(k_plan_smem<MAXN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    k_plan_smem<MAXN><<<P.S, SMEM_WARPS * 32, bytes, st>>>(P);
+  }
   launch_place<MAXN>(P, st);
 }
 

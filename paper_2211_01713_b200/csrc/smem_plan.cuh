@@ -308,7 +308,7 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
     slack_move_down(X.sj, X.spos, X.sdesc, X.sE, j, desc, cap - occ_old, cap - part, lane);
 }
 
-template <int MAXN>
+template <int MAXN, bool HWS = false>
 __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) {
   constexpr unsigned NO_KEY = 0xffffffffu;
   constexpr unsigned FULL = 0xffffffffu;
@@ -317,10 +317,14 @@ __global__ void __launch_bounds__(SMEM_WARPS * 32, 1) k_plan_smem(PlanParams P) 
   const int t = threadIdx.x, lane = t & 31, wi = t >> 5;
   const int s = blockIdx.x;
   Hand *const hdp = P.hand + s;
-  __shared__ Hw shw;  // the scenario's profile (IGP_F_HWS: one per scenario)
-  if (t == 0) shw = P.hw_s ? P.hw_s[s] : P.hw;
-  __syncthreads();
-  const Hw &hw = shw;
+  // the profile: the launch's (constant bank), or the scenario's (IGP_F_HWS,
+  // staged in shared memory)
+  __shared__ Hw shw[HWS ? 1 : 1];
+  if constexpr (HWS) {
+    if (t == 0) shw[0] = P.hw_s[s];
+    __syncthreads();
+  }
+  const Hw &hw = HWS ? shw[0] : P.hw;
   const int m = P.m, cap = hw.cap;
   if (P.perr[s] != INT_MAX || P.sflags[s] != 0 || !hw.margin_ok) {
     if (t == 0) hdp->k_done = P.k0;  // declined: k_place plans it
