@@ -112,7 +112,7 @@ enum {
   IGP_F_NO_PRED = 2,    /* skip the _build_plan breakdown rows */
   IGP_F_SMEM = 8,       /* with IGP_F_CTA: one CTA per scenario keeps the search
                            state in shared memory and evaluates each candidate
-                           with one warp (csrc/smem_plan.cuh; up to about 1,900
+                           with one warp (csrc/smem_plan.cuh; up to about 1,250
                            workloads, larger scenarios use the per-CTA kernel);
                            falls back on the device like IGP_F_COOP */
   IGP_F_CTA = 4,        /* one CTA (many warps) per scenario instead of one warp:

@@ -1,5 +1,5 @@
 // smem_plan.cuh -- one plan per CTA with the scenario's search state in shared
-// memory (single plans of up to about 1,900 workloads: BASELINE C1/C2).
+// memory (single plans of up to about 1,250 workloads: BASELINE C1/C2).
 //
 // A single plan is a chain of m dependent steps (planner.py:290-319); the
 // per-step latency is what a user waits for.  k_place<.., 8> keeps the state in
