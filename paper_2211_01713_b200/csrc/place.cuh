@@ -518,6 +518,32 @@ __device__ __forceinline__ Solo solo_lookup(const double *tbl, const double *col
   return solo_from_cold(cold + (size_t)k * C_NF, (double)u * hw.runit);
 }
 
+// Solo terms at L consecutive units u, u+1, ... in one round trip: when they
+// are all inside the workload's table row, every 16-byte load is issued before
+// any is used (a chain of solo_lookup calls compiles to one dependent table
+// load after another); otherwise one solo_lookup per unit.
+template <int L>
+__device__ __forceinline__ void solo_run(const double *tbl, const double *cold, const Hw &hw, int k,
+                                         int lb, int u, Solo *out) {
+  const int v = u - lb;
+  if (v >= 0 && v + L - 1 < TB && u + L - 1 <= hw.cap) {
+    const double2 *t = reinterpret_cast<const double2 *>(tbl + ((size_t)k * TB + v) * 4);
+    double2 q[2 * L];
+#pragma unroll
+    for (int i = 0; i < 2 * L; ++i) q[i] = t[i];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      out[i].ka = q[2 * i].x;
+      out[i].pw = q[2 * i].y;
+      out[i].ca = q[2 * i + 1].x;
+      out[i].err = (int)q[2 * i + 1].y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < L; ++i) out[i] = solo_lookup(tbl, cold, hw, k, lb, u + i);
+  }
+}
+
 struct ErrOut {
   int code, k;
   double a, b, c;
@@ -813,8 +839,9 @@ __device__ __forceinline__ void commit_step(const PlanParams &P, const Hw &hw, c
             f_ca = fv.y;
           }
           if (nu != (int)mt.u) {
-            const Solo so = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu);
-            const Solo s1 = solo_lookup(tbl, cold, hw, mt.k, mt.lb, nu + 1);
+            Solo sr[2];
+            solo_run<2>(tbl, cold, hw, mt.k, mt.lb, nu, sr);
+            const Solo so = sr[0], s1 = sr[1];
             rr[R_KA] = so.ka;
             rr[R_CA] = so.ca;
             rr[R_PW] = so.pw;

@@ -140,6 +140,9 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
   const int cap = hw.cap;
   const double n_ka = NB.nw[R_KA], n_ca = NB.nw[R_CA], n_pw = NB.nw[R_PW];
   const double ksch = NB.cold[C_KSCH], nkern = NB.cold[C_NK];
+#if IGP_TIMING
+  const long long c0 = clock64();
+#endif
   int j, n_old, occ_old, off;
   if (bk == NO_KEY) {
     j = G;
@@ -223,9 +226,11 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
         s2 = at(v + 2, nu + 2);
       } else {
         const int lb = X.slb[kk];
-        so = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu);
-        s1 = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu + 1);
-        s2 = solo_lookup(Z.tbl, Z.cold, hw, kk, lb, nu + 2);
+        Solo sr[3];
+        solo_run<3>(Z.tbl, Z.cold, hw, kk, lb, nu, sr);
+        so = sr[0];
+        s1 = sr[1];
+        s2 = sr[2];
       }
       X.ska2[kk] = s2.ka;
       X.cd2[kk] = make_double2(s2.ca - s1.ca, s2.pw - s1.pw);
@@ -265,6 +270,9 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
   }
   part = warp_sum(part);
   __syncwarp();
+#if IGP_TIMING
+  const long long c1 = clock64();
+#endif
   // exact prefix fold states of this GPU, in resident order (model.py:299/304)
   Neumaier fp, fc;
   fp.s = fp.c = fc.s = fc.c = 0.0;  // as commit_step (an add from zero is Neumaier.first)
@@ -288,6 +296,9 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
     fp.add(pw);
     fc.add(ca);
   }
+#if IGP_TIMING
+  const long long c2 = clock64();
+#endif
   const unsigned long long desc = ((unsigned long long)off << 32) | (unsigned)part | ((unsigned)n << 16);
   if (lane == 0) {
     double *gf = Z.gfold + (size_t)j * 4;
@@ -306,6 +317,14 @@ __device__ __forceinline__ void commit_smem(const PlanParams &P, const Hw &hw, c
     slack_insert(X.sj, X.spos, X.sdesc, X.sE, j, desc, cap - need, lane);
   else
     slack_move_down(X.sj, X.spos, X.sdesc, X.sE, j, desc, cap - occ_old, cap - part, lane);
+#if IGP_TIMING
+  if (lane == 0 && blockIdx.x == 0 && P.stats) {
+    const long long c3 = clock64();
+    atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 4], (unsigned long long)(c1 - c0));
+    atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 5], (unsigned long long)(c2 - c1));
+    atomicAdd((unsigned long long *)&P.stats[IGP_NSTAT * P.S + 6], (unsigned long long)(c3 - c2));
+  }
+#endif
 }
 
 template <int MAXN, bool HWS = false>

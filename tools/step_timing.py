@@ -19,7 +19,7 @@ if S == 0:
 wl, names = synth.scenarios(S, m, hw, seed=2211, **kw)
 d_wl = torch.from_numpy(wl).cuda(); d_rk = torch.from_numpy(name_ranks(list(names))).cuda()
 i32 = torch.empty((5, S, m), dtype=torch.int32, device="cuda")
-gc = torch.empty(S, dtype=torch.int32, device="cuda"); st = torch.zeros(6 * S + 10, dtype=torch.int64, device="cuda")
+gc = torch.empty(S, dtype=torch.int32, device="cuda"); st = torch.zeros(6 * S + 12, dtype=torch.int64, device="cuda")
 er = torch.empty((S, 40), dtype=torch.uint8, device="cuda")
 ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, bm, fl), dtype=torch.uint8, device="cuda")
 for rep in range(2):
@@ -29,7 +29,7 @@ for rep in range(2):
                                    P(ws), ws.numel(), fl, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
 t = st.cpu().numpy()[6 * S:6 * S + 4] / m
-extra = st.cpu().numpy()[6 * S + 4:6 * S + 6]
+extra = (st.cpu().numpy()[6 * S + 4:6 * S + 7] / m).round().tolist()
 print(f"S={S} m={m} flags={fl}: cycles/step start+newcomer {t[0]:.0f} | candidates {t[1]:.0f} | "
       f"post-candidates {t[2]:.0f} | commit {t[3]:.0f} | total {t.sum():.0f} ({t.sum()/1.965e3:.2f} us @1.965GHz)"
-      f" | counters {extra.tolist()}")
+      f" | extra per step {extra}")
