@@ -39,7 +39,6 @@
 namespace igp {
 
 constexpr double FAST_DELTA = 0x1p-30;    // decision margin, relative to beta
-constexpr double FAST_MAX_ACACHE = 16.0;  // SF_NO_FAST above this alpha_cache
 enum { R_EXACT = 4 };
 
 __device__ __forceinline__ double fast_beta(double thalf, double tload, double tfb) {

@@ -59,6 +59,8 @@ enum { R_KA = 0, R_CA, R_TSN, R_ACACHE, R_TLOAD, R_TFB, R_THALF, R_PW, R_KA1, R_
        R_ERR1, R_NF };
 #endif
 enum { SF_RISKY = 1, SF_NO_MARGIN = 2, SF_NO_FAST = 4 };
+// the certified-margin kernels' error bound assumes alpha_cache <= this (fast.cuh)
+constexpr double FAST_MAX_ACACHE = 16.0;
 enum { R_FEAS = 0, R_INFEAS = 1, R_PRUNED = 2, R_ERROR = 3 };
 
 struct Meta {
@@ -371,8 +373,8 @@ __global__ void k_prologue_plan(PlanParams P) {
       !(cold[C_NK] >= 0.0) || !(slot[S_ACACHE] >= 0.0) || !(slot[S_ACACHE] <= 1e6) ||
       !isfinite(slot[S_TLOAD] + slot[S_TFB] + slot[S_THALF] + cold[C_KSCH] * cold[C_NK]))
     fl |= SF_NO_MARGIN;
-  // the fast kernel's error bound assumes alpha_cache <= FAST_MAX_ACACHE (fast.cuh)
-  if (!(slot[S_ACACHE] <= 16.0)) fl |= SF_NO_FAST;
+  // the certified-margin kernels' error bound assumes alpha_cache <= FAST_MAX_ACACHE
+  if (!(slot[S_ACACHE] <= FAST_MAX_ACACHE)) fl |= SF_NO_FAST;
   if (!(u <= 0xffff)) fl |= SF_RISKY;
   if (P.stream) P.code[o] = fl << 8;
   else if (fl) atomicOr(&P.sflags[s], fl);
