@@ -54,7 +54,7 @@ FLOPS_PER_EVAL_CALL = 9     # fp64 ops per device evaluation
 # and its two Neumaier fold states (8 + 32 B)
 BYTES_PER_RESIDENT_READ = 64
 BYTES_PER_TRIAL = 40
-KERNELS_PER_PLAN_CALL = 6   # k_fill_int, k_prologue_plan, k_sort, k_build, k_table, k_place
+KERNELS_PER_PLAN_CALL = 7   # k_fill_int, k_prologue_plan, k_sort, k_build, k_table, k_place (lean + full pass)
 
 
 def parse():

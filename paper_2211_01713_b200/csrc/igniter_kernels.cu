@@ -413,10 +413,10 @@ static DevOcc dev_occupancy(Kern kern, int threads, size_t smem) {
 #define IGP_MINB_BIG 5  // resident CTAs per SM of the large-plan one-warp build
 #endif
 
-template <int MAXN, int GW, bool HWS = false, int MINB = 0>
+template <int MAXN, int GW, bool HWS = false, int MINB = 0, bool LEAN = false>
 static unsigned place_grid(int S) {
   // persistent launch: at most as many groups as can be co-resident
-  const DevOcc o = dev_occupancy(k_place<MAXN, GW, false, HWS, MINB>, GW == 1 ? 128 : GW * 32,
+  const DevOcc o = dev_occupancy(k_place<MAXN, GW, false, HWS, MINB, LEAN>, GW == 1 ? 128 : GW * 32,
                                  place_smem<GW>());
   const int gpb = (GW == 1) ? 4 : 1;
   const long long want = (S + gpb - 1) / gpb;
@@ -441,6 +441,17 @@ static void launch_place(const PlanParams &P, cudaStream_t st) {
     k_place_fast<MAXN><<<fast_grid<MAXN>(P.S), 128, fast_smem(), st>>>(P);
   }
   cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
+  if (P.hand && !P.crec && !P.hw_s && !(P.flags & (IGP_F_CTA | IGP_F_GW2 | IGP_F_GW4 | IGP_F_SMEM))) {
+    // the lean pass (no exact-sequence code), then the full pass below plans
+    // only the scenarios it declined
+    if (P.m >= IGP_MINB5_FROM_M && MAXN == 48)
+      k_place<MAXN, 1, false, false, IGP_MINB_BIG, true>
+          <<<place_grid<MAXN, 1, false, IGP_MINB_BIG, true>(P.S), 128, place_smem<1>(), st>>>(P);
+    else
+      k_place<MAXN, 1, false, false, 0, true>
+          <<<place_grid<MAXN, 1, false, 0, true>(P.S), 128, place_smem<1>(), st>>>(P);
+    cudaMemsetAsync(P.sched, 0, sizeof(int32_t), st);
+  }
   if (P.hw_s) {  // one profile per scenario: one CTA or one warp per scenario
     if (P.flags & IGP_F_CTA)
       k_place<MAXN, 8, false, true>
@@ -651,7 +662,8 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   const bool smem = !fast && !P.coop && (flags & IGP_F_SMEM) && (flags & IGP_F_CTA) &&
                     !(flags & IGP_F_STATS) && L.total > L.hand && m > 0 &&
                     smem_need <= smem_plan_limit();
-  P.hand = (fast || smem) ? (Hand *)(ws + L.hand) : nullptr;
+  const bool lean = !fast && !smem && !P.coop && lean_path(flags) && L.total > L.hand;
+  P.hand = (fast || smem || lean) ? (Hand *)(ws + L.hand) : nullptr;
   // the fast kernel's decision margin; IGP_FAST_DELTA raises it (tests force the
   // exact fallback with it); it is never lowered below FAST_DELTA
   P.fast_delta = FAST_DELTA;
@@ -713,7 +725,7 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
       else if (hw.cap <= 128) rc = launch_place_coop<128>(P, st);
       else rc = launch_place_coop<256>(P, st);
       if (rc) return rc;
-    } else if (P.hand && !P.crec) {  // IGP_F_SMEM
+    } else if (P.hand && (flags & IGP_F_SMEM)) {  // the shared-memory plan kernel
       const size_t bytes = smem_layout(m, P.pool_recs, hw.cap).total;
       if (hw.cap <= 48) launch_smem<48>(P, bytes, st);
       else if (hw.cap <= 128) launch_smem<128>(P, bytes, st);

@@ -205,6 +205,7 @@ struct __align__(16) FastSlot {
 // Hand-off from k_place_fast to k_place (which writes the plan and the
 // _build_plan rows): the step where k_place resumes (k1 = all planned, k0 =
 // declined) and the scenario state after the fast steps.
+constexpr int HAND_COMPLETE = 0x7fffffff;  // k_done of a scenario the lean pass planned
 struct Hand {
   int k_done, G, pool_top, abort;
   unsigned long long evals_run, cands_run, exact_run, pad;
@@ -231,6 +232,16 @@ static int pool_factor(int flags) {
 static bool fast_path(int flags) {
   return (flags & IGP_F_FAST) && !(flags & (IGP_F_STATS | IGP_F_CTA | IGP_F_GW2 | IGP_F_GW4 |
                                             IGP_F_COOP | IGP_F_WIN | IGP_F_HWS));
+}
+
+// The batch path of one-warp scenarios runs the lean pass first (k_place LEAN).
+static bool lean_path(int flags) {
+#ifdef IGP_NO_LEAN
+  return false;
+#else
+  return !(flags & (IGP_F_FAST | IGP_F_STATS | IGP_F_CTA | IGP_F_GW2 | IGP_F_GW4 | IGP_F_COOP |
+                    IGP_F_WIN | IGP_F_HWS | IGP_F_SMEM));
+#endif
 }
 
 static WsLayout ws_layout(int S, int m, int cap, int flags) {
@@ -272,7 +283,8 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const bool fast = fast_path(flags);
   L.crec = off; off = align_up(off + (fast ? Sp * sizeof(CRec) : 0));
   L.cnext = off; off = align_up(off + (fast ? Sp * sizeof(CNext) : 0));
-  L.hand = off; off = align_up(off + ((fast || (flags & IGP_F_SMEM)) ? (size_t)S * sizeof(Hand) : 0));
+  L.hand = off;
+  off = align_up(off + ((fast || lean_path(flags) || (flags & IGP_F_SMEM)) ? (size_t)S * sizeof(Hand) : 0));
   L.total = off;
   return L;
 }
@@ -952,7 +964,12 @@ __device__ __forceinline__ void commit_step(const PlanParams &P, const Hw &hw, c
 // (20 warps/SM, 102 registers) for large plans, where more resident scenarios
 // hide more latency (+6.5% at 10k workloads); the default 4 (128 registers,
 // fewer spills) wins on short plans (1k workloads: 81k vs 76k plans/s).
-template <int MAXN, int GW, bool COOP = false, bool HWS = false, int MINB = 0>
+// LEAN: a batch pass compiled without the exact evaluation sequence (PlanStats,
+// inputs that can raise): those scenarios are left to a second, full pass
+// (Hand.k_done = k0); the rest are planned completely (k_done = HAND_COMPLETE).
+// The exact-sequence code no longer shares the hot loop's registers (spills
+// 172 instead of 400 bytes at 96 registers).
+template <int MAXN, int GW, bool COOP = false, bool HWS = false, int MINB = 0, bool LEAN = false>
 __global__ void __launch_bounds__(GW == 1 ? 128 : GW * 32,
                                   MINB ? MINB
                                        : GW == 1 ? IGP_MINB_WARP
@@ -1014,6 +1031,19 @@ k_place(PlanParams P) {
   const int m = P.m, cap = hw.cap;
   const size_t sm = (size_t)s * m;
   igp_error *err = P.err + s;
+
+  if constexpr (!COOP) {
+    if (P.hand) {
+      if constexpr (LEAN) {  // the exact sequence is the full pass's
+        const bool decline =
+            P.perr[s] != INT_MAX || (P.sflags[s] & SF_RISKY) || (P.flags & IGP_F_STATS);
+        if (t == 0) P.hand[s].k_done = decline ? P.k0 : HAND_COMPLETE;
+        if (decline) continue;
+      } else if (ld_cg(&P.hand[s].k_done) == HAND_COMPLETE) {
+        continue;  // planned by the lean pass
+      }
+    }
+  }
 
   if (!P.stream && P.perr[s] != INT_MAX) {  // prologue error, input order (planner.py:280-282)
     if (t == 0) {
@@ -1079,7 +1109,7 @@ k_place(PlanParams P) {
   // steps the certified-margin fast kernel ran (fast.cuh): plan mode, all of
   // them or none; the predictions and outputs below remain
   const Hand *const hdp = (!COOP && P.hand) ? P.hand + s : nullptr;
-  const bool fast_done = hdp && !coop_done && hdp->k_done > P.k0;
+  const bool fast_done = !LEAN && hdp && !coop_done && hdp->k_done > P.k0;
   if (fast_done) k_coop = hdp->k_done;
   const bool resumed = coop_done || fast_done;
   const unsigned lt = (1u << lane) - 1u;
@@ -1137,7 +1167,7 @@ k_place(PlanParams P) {
         break;
       }
     }
-    const bool exact = (P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY);
+    const bool exact = !LEAN && ((P.flags & IGP_F_STATS) || ((sflags | aflags) & SF_RISKY));
     const bool margin_rt = !((sflags | aflags) & SF_NO_MARGIN) && hw.margin_ok;
     // the newcomer (planner.py:291-292)
 #if IGP_TIMING
@@ -1664,9 +1694,14 @@ k_place(PlanParams P) {
       }
     };
 
-    if (exact) run_step(BoolC<false>{}, BoolC<true>{}, IntC<2>{});
-    else if (margin_rt) run_step(BoolC<false>{}, BoolC<false>{}, IntC<1>{});
-    else run_step(BoolC<false>{}, BoolC<false>{}, IntC<0>{});
+    if constexpr (!LEAN) {
+      if (exact) run_step(BoolC<false>{}, BoolC<true>{}, IntC<2>{});
+      else if (margin_rt) run_step(BoolC<false>{}, BoolC<false>{}, IntC<1>{});
+      else run_step(BoolC<false>{}, BoolC<false>{}, IntC<0>{});
+    } else {
+      if (margin_rt) run_step(BoolC<false>{}, BoolC<false>{}, IntC<1>{});
+      else run_step(BoolC<false>{}, BoolC<false>{}, IntC<0>{});
+    }
 #if IGP_TIMING
     long long tm2 = clock64();
 #endif
@@ -1675,11 +1710,12 @@ k_place(PlanParams P) {
     n_ready = true;
     n_phase ^= 1u;
 
-    if (gs.err_flag) {
+    if (!LEAN && gs.err_flag) {
       // exact mode only: replay the step in the reference's candidate order to
       // find the first raising candidate and the PlanStats at that point
       st_evals = st_calls = st_cands = st_rres = st_run = 0;
-      if (wi == 0) run_step(BoolC<true>{}, BoolC<true>{}, IntC<2>{});
+      if constexpr (!LEAN)
+        if (wi == 0) run_step(BoolC<true>{}, BoolC<true>{}, IntC<2>{});
       if (t != 0) st_evals = st_calls = st_cands = st_rres = st_run = 0;
       tot_evals += st_evals;
       tot_calls += st_calls;
