@@ -1,15 +1,18 @@
 #!/bin/bash
 # Round-end evidence: GPU suite + smoke, the bench line (default: two waves) and
-# the reference arm, the ncu launch list of the bench command, and the DRAM
-# traffic of one k_place launch at the bench batch (targeted ncu metrics).
+# the reference arm, the config sweep, the ncu launch list of the bench command,
+# and the DRAM traffic of one k_place launch at the bench batch (targeted ncu metrics).
 OUT=gpurun_out/${1:-final}; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
-timeout 1800 python -m pytest tests -q -m gpu --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+if [ "$2" != "skip-tests" ]; then
+  timeout 1800 python -m pytest tests -q -m gpu --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+fi
 timeout 1200 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 1500 python tools/bench_configs.py > $OUT/configs.jsonl 2> $OUT/configs.err; echo "configs rc=$?" >> $OUT/configs.err
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --check 0 > $OUT/ncu_bench.log 2>&1
 timeout 1800 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:k_place -s 1 -c 1 --csv --log-file $OUT/traffic.csv python tools/profile_place.py 5920 10000 0 > $OUT/ncu_traffic.log 2>&1
+  -k regex:k_place -s 2 -c 1 --csv --log-file $OUT/traffic.csv python tools/profile_place.py 5920 10000 0 > $OUT/ncu_traffic.log 2>&1
 echo done > $OUT/DONE
