@@ -653,16 +653,16 @@ static int plan_device_impl(const double *wl, int n_scen, int m, const double *h
   P.sE = (int32_t *)(ws + L.sE);
   P.nxt = (double *)(ws + L.nxt);
   // the layout (sized with the caller's flags) holds the compact tiles
-  const bool fast = L.total > L.hand && fast_path(flags) && !P.coop;
+  const bool fast = L.cnext > L.crec && fast_path(flags) && !P.coop;
   P.crec = fast ? (CRec *)(ws + L.crec) : nullptr;
   P.cnext = fast ? (CNext *)(ws + L.cnext) : nullptr;
   // IGP_F_SMEM: the shared-memory plan kernel when the scenario's state fits
   const size_t smem_need =
       smem_layout(m, L.pool_recs, hw.cap).total;
   const bool smem = !fast && !P.coop && (flags & IGP_F_SMEM) && (flags & IGP_F_CTA) &&
-                    !(flags & IGP_F_STATS) && L.total > L.hand && m > 0 &&
+                    !(flags & IGP_F_STATS) && m > 0 &&
                     smem_need <= smem_plan_limit();
-  const bool lean = !fast && !smem && !P.coop && lean_path(flags) && L.total > L.hand;
+  const bool lean = !fast && !smem && !P.coop && lean_path(flags);
   P.hand = (fast || smem || lean) ? (Hand *)(ws + L.hand) : nullptr;
   // the fast kernel's decision margin; IGP_FAST_DELTA raises it (tests force the
   // exact fallback with it); it is never lowered below FAST_DELTA

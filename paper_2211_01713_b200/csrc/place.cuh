@@ -283,8 +283,10 @@ static WsLayout ws_layout(int S, int m, int cap, int flags) {
   const bool fast = fast_path(flags);
   L.crec = off; off = align_up(off + (fast ? Sp * sizeof(CRec) : 0));
   L.cnext = off; off = align_up(off + (fast ? Sp * sizeof(CNext) : 0));
-  L.hand = off;
-  off = align_up(off + ((fast || lean_path(flags) || (flags & IGP_F_SMEM)) ? (size_t)S * sizeof(Hand) : 0));
+  // the hand-off records (lean pass, certified-margin and shared-memory
+  // kernels) are always laid out: S x 48 bytes, so that a workspace sized
+  // for one set of flags (e.g. with IGP_F_STATS) serves the others
+  L.hand = off; off = align_up(off + (size_t)S * sizeof(Hand));
   L.total = off;
   return L;
 }

@@ -64,7 +64,8 @@ class DevicePlan:
         self.gc = torch.empty(S, dtype=torch.int32, device=dev)
         self.st = torch.empty((S, 6), dtype=torch.int64, device=dev)
         self.err = torch.empty((S, 40), dtype=torch.uint8, device=dev)
-        self.ws = torch.empty(_device.plan_workspace_bytes(S, m, hv, b_max, flags | IGP_F_STATS),
+        self.ws = torch.empty(max(_device.plan_workspace_bytes(S, m, hv, b_max, fl)
+                                  for fl in (flags, flags | IGP_F_STATS)),
                               dtype=torch.uint8, device=dev)
 
     def run(self, flags=None):
