@@ -41,7 +41,7 @@ constexpr int TILE0 = 4;   // initial tile capacity
 #define IGP_PF_BATCH 0  // L2 prefetch of the next refill batch's tiles
 #endif
 #ifndef IGP_NW_SMEM
-#define IGP_NW_SMEM 0  // newcomer record in shared memory (register-pressure variant)
+#define IGP_NW_SMEM 1  // newcomer record in shared memory (frees registers: +2.5% at 10k with the lean pass)
 #endif
 #ifndef IGP_PF_DESC
 #define IGP_PF_DESC 1  // L1 prefetch of the next refill's slack-order descriptors
